@@ -1,0 +1,39 @@
+# Builds the product library (host C++ + sm_100a CUDA, C-ABI in
+# include/cobs_gpu.h) and the test-only CPU oracle (oracle/Makefile).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+           -Xcudafe --diag_suppress=177
+SRC := paper_1905_09624_b200/csrc
+OUT := paper_1905_09624_b200/_lib
+OBJS := $(OUT)/host.o $(OUT)/index.o $(OUT)/query.o $(OUT)/build.o $(OUT)/capi.o
+HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh $(SRC)/*.h) include/cobs_gpu.h
+
+.PHONY: all lib oracle clean
+all: lib oracle
+lib: $(OUT)/libcobs_gpu.so $(OUT)/libcobs_synth.so
+
+$(OUT)/libcobs_synth.so: $(SRC)/synth_host.c $(SRC)/synth.h
+	@mkdir -p $(OUT)
+	gcc -std=gnu11 -O2 -fPIC -shared -pthread -o $@ $(SRC)/synth_host.c -lm
+
+$(OUT)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OUT)/host.o: $(SRC)/host.cpp $(HDRS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
+
+$(OUT)/capi.o: $(SRC)/capi.cpp $(HDRS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(OUT)/libcobs_gpu.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(OUT) oracle/_build

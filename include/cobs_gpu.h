@@ -1,0 +1,198 @@
+/* cobs_gpu.h — C-ABI of the B200-native COBS query / construction path.
+ *
+ * This is the drop-in boundary.  The reference exposes its path as a C++ API
+ * (/root/reference/proj/include/cobs); every entry point below names the
+ * reference interface it replaces.  Plain pointers and sizes only: no C++ or
+ * torch types cross this boundary, no exceptions escape it.
+ *
+ * Return codes mirror the reference's exception taxonomy as its CLI maps
+ * it (proj/src/cli.cpp:448-454):
+ *   COBS_OK (0)     success
+ *   COBS_EUSAGE (1) std::invalid_argument  (bad K, bad params, ...)
+ *   COBS_EDATA (2)  cobs::DataError        (corrupt file, empty corpus,
+ *                                           duplicate names, l = 0 pattern)
+ *   COBS_ECUDA (4)  device failure (no reference equivalent)
+ * Error text (same wording as the reference's exception messages) goes to
+ * `err` (may be NULL) truncated to `errlen`.
+ *
+ * Threading: one CUDA stream per index handle; calls on one handle are
+ * serialised by the library; distinct handles are independent.  Results are
+ * library-allocated and freed by the library.
+ */
+#ifndef COBS_GPU_H
+#define COBS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COBS_OK 0
+#define COBS_EUSAGE 1
+#define COBS_EDATA 2
+#define COBS_ECUDA 4
+
+#define COBS_KIND_CLASSIC 0 /* proj/include/cobs/index_view.hpp:13 */
+#define COBS_KIND_COMPACT 1 /* proj/include/cobs/index_view.hpp:14 */
+
+/* proj/include/cobs/params.hpp:17-38 (IndexParams) */
+typedef struct cobs_index_params {
+    uint32_t q;
+    uint32_t k;
+    double p;
+    uint64_t block_size;
+    uint8_t canonical;
+    uint8_t hash_scheme;
+    uint8_t reserved[6];
+} cobs_index_params;
+
+typedef struct cobs_gpu_index cobs_gpu_index;
+typedef struct cobs_gpu_results cobs_gpu_results;
+
+/* ---- library ---------------------------------------------------------- */
+
+/* Version string of this library. */
+const char* cobs_gpu_version(void);
+
+/* ---- index lifecycle -------------------------------------------------- */
+
+/* Replaces cobs::open_resident (proj/include/cobs/storage.hpp:19,
+ * proj/src/storage.cpp:407-411): parse + validate with the same rejection
+ * matrix as parse_index (proj/src/storage.cpp:182-280), then upload every
+ * block payload to HBM on `device` (rows re-pitched to 32-byte multiples). */
+int cobs_gpu_index_open(const char* path, int device, cobs_gpu_index** out, char* err,
+                        size_t errlen);
+
+/* Same, from an in-memory file image (`path` is only used in messages). */
+int cobs_gpu_index_open_image(const uint8_t* image, uint64_t len, const char* path, int device,
+                              cobs_gpu_index** out, char* err, size_t errlen);
+
+/* Releases HBM and host state.  NULL is a no-op. */
+void cobs_gpu_index_close(cobs_gpu_index* index);
+
+/* IndexView metadata (proj/include/cobs/index_view.hpp:22-35). */
+int cobs_gpu_index_params(const cobs_gpu_index* index, cobs_index_params* out);
+uint8_t cobs_gpu_index_kind(const cobs_gpu_index* index);
+uint64_t cobs_gpu_index_block_count(const cobs_gpu_index* index);
+uint64_t cobs_gpu_index_doc_count(const cobs_gpu_index* index, uint64_t block);
+uint64_t cobs_gpu_index_width(const cobs_gpu_index* index, uint64_t block);
+uint64_t cobs_gpu_index_row_bytes(const cobs_gpu_index* index, uint64_t block);
+uint64_t cobs_gpu_index_total_docs(const cobs_gpu_index* index);
+/* IndexView::doc(b, i) (index_view.hpp:27).  `name` stays valid until close. */
+int cobs_gpu_index_doc(const cobs_gpu_index* index, uint64_t block, uint64_t i, const char** name,
+                       uint64_t* name_len, uint64_t* term_count);
+/* Global column (file column order, block-major) of document (block, i). */
+uint64_t cobs_gpu_index_doc_global(const cobs_gpu_index* index, uint64_t block, uint64_t i);
+/* HBM bytes held by the payload (pitched) and by the whole index. */
+uint64_t cobs_gpu_index_device_bytes(const cobs_gpu_index* index);
+/* IndexView::row_data (index_view.hpp:41-42) served from HBM by a D2H copy of
+ * bytes [byte_lo, byte_hi) of row r (slow; tools and tests). */
+int cobs_gpu_index_row(const cobs_gpu_index* index, uint64_t block, uint64_t r, uint64_t byte_lo,
+                       uint64_t byte_hi, uint8_t* out);
+/* Replaces cobs::write_index(const IndexView&, path) (storage.hpp:14,
+ * proj/src/storage.cpp:345-397) for a device-resident index: the payload is
+ * read back from HBM and the file is byte-identical to the reference's. */
+int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* err, size_t errlen);
+
+/* ---- batch query ------------------------------------------------------ */
+
+/* flags */
+#define COBS_Q_HITS 1u          /* ordered, thresholded hit lists */
+#define COBS_Q_SCORES 2u        /* dense per-document score matrix n x total_docs */
+#define COBS_Q_DEVICE_INPUT 4u  /* patterns / offsets are device pointers */
+#define COBS_Q_KEEP_DEVICE 8u   /* leave results in HBM (no D2H); for timing */
+
+/* Replaces cobs::query (proj/include/cobs/query.hpp:46-47,
+ * proj/src/query.cpp:123-164) over a batch, the way the CLI batch mode
+ * calls it (proj/src/cli.cpp:205-221): query i is pattern bytes
+ * [offsets[i], offsets[i+1]).  Patterns are raw bytes (not uppercased), as
+ * query() takes them.  K outside (0,1] -> COBS_EUSAGE for the whole batch
+ * (query.cpp:125-126); a pattern with l = 0 gets status COBS_EDATA and the
+ * reference's message in its result (query.cpp:133-138), as the CLI's inline
+ * "ERR" line does, and does not abort the batch. */
+int cobs_gpu_query_batch(cobs_gpu_index* index, const uint8_t* patterns, const uint64_t* offsets,
+                         uint64_t n, double K, uint64_t top_t, uint32_t flags,
+                         cobs_gpu_results** out, char* err, size_t errlen);
+
+uint64_t cobs_gpu_results_count(const cobs_gpu_results* r);
+/* QueryResult fields (query.hpp:31-39) of query i: ell, skipped, status
+ * (0 / COBS_EDATA), message (empty when ok), number of hits after top_t. */
+int cobs_gpu_results_query(const cobs_gpu_results* r, uint64_t i, uint64_t* ell, uint64_t* skipped,
+                           int* status, const char** message, uint64_t* n_hits);
+/* Hits of query i ordered by (score desc, name asc) (query.cpp:156-162):
+ * global document columns and scores.  Pointers valid until free. */
+int cobs_gpu_results_hits(const cobs_gpu_results* r, uint64_t i, const uint32_t** docs,
+                          const uint32_t** scores);
+/* Bulk view of all n queries (for array-oriented hosts): ell[n], skipped[n],
+ * status[n], hit_off[n] / hit_n[n] index into doc/score[total_hits]. */
+int cobs_gpu_results_arrays(const cobs_gpu_results* r, const uint32_t** ell, const uint64_t** skipped,
+                            const int** status, const uint64_t** hit_off, const uint64_t** hit_n,
+                            const uint32_t** docs, const uint32_t** scores, uint64_t* total_hits);
+/* Dense score matrix (COBS_Q_SCORES): n x total_docs values of
+ * `*score_bytes` (2 when every l <= 65535, else 4, as query.cpp:150-153
+ * picks uint16/uint32 counters), row i = query i, columns in file order. */
+const void* cobs_gpu_results_scores(const cobs_gpu_results* r, uint32_t* score_bytes);
+/* Device-side timings of the batch (ms, CUDA events on the index's stream):
+ * termize+hash, gather, order, and the whole call from before the H2D of
+ * the patterns to after the D2H of the results. */
+int cobs_gpu_results_timing(const cobs_gpu_results* r, double* ms_termize, double* ms_gather,
+                            double* ms_order, double* ms_total);
+/* Kernels of this library launched by the batch (library sorts excluded). */
+uint32_t cobs_gpu_results_launches(const cobs_gpu_results* r);
+/* Algorithmic row bytes of the batch: sum_i k * l_i * sum_b row_bytes_b
+ * (the random-access reader's bytes_read accounting, storage.cpp:325-331). */
+uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r);
+void cobs_gpu_results_free(cobs_gpu_results* r);
+
+/* ---- build ------------------------------------------------------------ */
+
+/* Replaces extract_terms + build_classic / build_compact + write_index
+ * (termizer.hpp:37-38, classic_index.hpp:37-44, compact_index.hpp:26-27,
+ * storage.hpp:14-16).  Content strings i are bytes [seg_offsets[i],
+ * seg_offsets[i+1]) of `seqs`; document d owns strings
+ * [doc_segs[d], doc_segs[d+1]) (grams never span strings); names[d] is a
+ * NUL-terminated name.  kind: COBS_KIND_CLASSIC (documents in input order,
+ * width forced_w or sized for the largest document) or COBS_KIND_COMPACT
+ * (sorted by (term_count, name), blocks of block_size).  The image written
+ * to `out_path` (if non-NULL) and/or returned through `image`/`image_len`
+ * (if non-NULL; free with cobs_gpu_free) is byte-identical to the
+ * reference writer's. */
+int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_segs,
+                   const uint64_t* doc_segs, const char* const* names, uint64_t n_docs,
+                   const cobs_index_params* params, int kind, uint64_t forced_w, int device,
+                   const char* out_path, uint8_t** image, uint64_t* image_len, char* err,
+                   size_t errlen);
+
+/* Build timings (ms) of the calling thread's last cobs_gpu_build: term
+ * counting, fill (sequences in HBM -> finished matrix), total incl. H2D,
+ * D2H and serialisation. */
+int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total);
+
+void cobs_gpu_free(void* p);
+
+/* ---- synthetic workloads (bench / tests; not part of the reference
+ *      boundary) ----------------------------------------------------- */
+
+/* Config-5 procedural compact index generated directly in HBM from a seed
+ * (paper_1905_09624_b200/csrc/synth.h): n_docs documents with log-normal
+ * (median, sigma) term counts sorted into blocks of block_size, widths
+ * size_filter(block max, p, 1), i.i.d. Bernoulli bits of density
+ * 1-(1-1/w)^n per block.  Equivalent to opening the file the reference
+ * writer would produce for the same header and rows. */
+int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size, double median,
+                            double sigma, double p, int device, cobs_gpu_index** out, char* err,
+                            size_t errlen);
+
+/* Generate documents [doc_lo, doc_hi) of a synthetic corpus on the device
+ * into `dev_out` (device pointer, sum of lengths bytes, concatenated in
+ * document order). alpha: 0 DNA, 1 amino acids. */
+int cobs_gpu_synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo,
+                        uint64_t doc_hi, uint8_t* dev_out, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COBS_GPU_H */

@@ -1,0 +1,395 @@
+// Kernel 4: index construction on the device.
+//
+//   count pass  one thread per window (flattened over all documents, so
+//               skewed document sizes load-balance): canonicalise, XXH64,
+//               exact per-document distinct count through the lock-free set
+//               of dev.cuh -> term_count   (termizer.cpp:103-129,
+//               termizer.hpp:25)
+//   host        classic width / compact (term_count, name) sort, blocks of
+//               B, per-block widths        (classic_index.cpp:40-64,
+//               compact_index.cpp:19-52, bloom.cpp:50-66)
+//   fill pass   one thread per window and seed: atomicOr of bit
+//               (XXH64 % w_b, column) into the block's row-major matrix,
+//               stored unpitched at exactly the file's payload layout so the
+//               D2H copy IS the payload   (classic_index.cpp:26-36,
+//               bit_matrix.hpp:25-27).  OR is idempotent, so every window is
+//               filled, not just the distinct ones.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+
+#include "build.hpp"
+#include "dev.cuh"
+#include "index.hpp"
+#include "synth.h"
+
+namespace cobsg {
+
+namespace {
+
+thread_local BuildTiming g_timing;
+
+struct WinArgs {
+    const uint8_t* seqs;
+    const uint64_t* seg_off;   // n_segs+1 byte offsets into seqs
+    const uint64_t* seg_wbase; // n_segs+1 window prefix (this pass's range)
+    const uint32_t* seg_doc;   // document of each segment
+    const uint64_t* doc_start; // byte offset of each document's first segment
+    uint64_t seg_lo, seg_hi;   // segment range of this pass
+    uint64_t w_lo, w_hi;       // window range of this pass
+    uint32_t q, k;
+    int canonical;
+};
+
+// window g -> (segment, offset in segment)
+__device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
+    uint64_t lo = a.seg_lo, hi = a.seg_hi; // seg_wbase[lo] <= g < seg_wbase[hi]
+    while (hi - lo > 1) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (a.seg_wbase[mid] <= g)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long long* tab,
+                                                    const uint64_t* tab_off, const uint64_t* tab_slots,
+                                                    unsigned long long* term_count) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t base = a.w_lo + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32;
+         base < a.w_hi; base += warps * 32) {
+        uint64_t g = base + lane;
+        bool rep = false;
+        uint32_t doc = 0;
+        if (g < a.w_hi) {
+            uint64_t s = find_seg(a, g);
+            doc = a.seg_doc[s];
+            uint64_t pos = a.seg_off[s] + (g - a.seg_wbase[s]); // byte of window start
+            const uint8_t* dbase = a.seqs + a.doc_start[doc];
+            const uint8_t* w = a.seqs + pos;
+            bool valid = true, rc = false;
+            if (a.canonical) {
+                valid = window_acgt(w, a.q);
+                if (valid) rc = choose_rc(w, a.q);
+            }
+            if (valid) {
+                uint64_t h = xxh64_term(w, a.q, rc, 0);
+                rep = set_insert(tab + tab_off[doc], tab_slots[doc] - 1, h,
+                                 static_cast<uint32_t>(pos - a.doc_start[doc]), dbase, a.q,
+                                 a.canonical != 0, rc);
+            }
+        }
+        unsigned act = __ballot_sync(0xffffffffu, rep);
+        if (rep) {
+            unsigned peers = __match_any_sync(act, doc);
+            if (lane == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(term_count + doc, (unsigned long long)__popc(peers));
+        }
+    }
+}
+
+struct FillBlock {
+    uint64_t base; // payload byte offset of row 0 (file layout)
+    uint64_t w, magic, rb;
+};
+
+__global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* blocks,
+                                                   const uint32_t* doc_block, const uint32_t* doc_col,
+                                                   unsigned int* words) {
+    for (uint64_t g = a.w_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < a.w_hi;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t s = find_seg(a, g);
+        uint32_t doc = a.seg_doc[s];
+        const uint8_t* w = a.seqs + a.seg_off[s] + (g - a.seg_wbase[s]);
+        bool rc = false;
+        if (a.canonical) {
+            if (!window_acgt(w, a.q)) continue;
+            rc = choose_rc(w, a.q);
+        }
+        const FillBlock B = blocks[doc_block[doc]];
+        const uint32_t col = doc_col[doc];
+        for (uint32_t seed = 0; seed < a.k; ++seed) {
+            uint64_t r = fastmod(xxh64_term(w, a.q, rc, seed), B.w, B.magic);
+            uint64_t byte = B.base + r * B.rb + (col >> 3);
+            atomicOr(words + (byte >> 2), 1u << (((byte & 3) << 3) + (col & 7)));
+        }
+    }
+}
+
+inline uint64_t next_pow2(uint64_t x) {
+    uint64_t p = 2;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+} // namespace
+
+const BuildTiming& last_build_timing() { return g_timing; }
+
+std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, uint64_t n_segs,
+                                 const uint64_t* doc_segs, const std::vector<std::string>& names,
+                                 const Params& P, uint8_t kind, uint64_t forced_w, int device) {
+    auto t_start = std::chrono::steady_clock::now();
+    g_timing = BuildTiming();
+    P.validate();                                             // params.hpp:26-35
+    const uint64_t n_docs = names.size();
+    if (n_docs == 0) throw DataError("build: no documents"); // classic_index.cpp:44
+    if (kind != kKindClassic && kind != kKindCompact) throw UsageError("build: unknown index kind");
+    {
+        std::vector<const std::string*> sorted(n_docs);
+        for (uint64_t d = 0; d < n_docs; ++d) sorted[d] = &names[d];
+        std::sort(sorted.begin(), sorted.end(),
+                  [](const std::string* a, const std::string* b) { return *a < *b; });
+        for (uint64_t i = 1; i < n_docs; ++i)
+            if (*sorted[i - 1] == *sorted[i]) // classic_index.cpp:17-22
+                throw DataError("duplicate document name: " + *sorted[i]);
+    }
+    for (uint64_t d = 0; d < n_docs; ++d)
+        if (doc_segs[d + 1] < doc_segs[d] || doc_segs[d + 1] > n_segs)
+            throw UsageError("build: bad document segment ranges");
+    if (doc_segs[0] != 0 || doc_segs[n_docs] != n_segs)
+        throw UsageError("build: document segment ranges must cover all segments in order");
+    const uint32_t q = P.q;
+
+    COBS_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    COBS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+
+    // windows per segment / document
+    std::vector<uint64_t> seg_wbase(n_segs + 1, 0), doc_start(n_docs), doc_w(n_docs, 0);
+    std::vector<uint32_t> seg_doc(n_segs);
+    for (uint64_t d = 0; d < n_docs; ++d) {
+        doc_start[d] = n_segs ? seg_off[doc_segs[d]] : 0;
+        for (uint64_t s = doc_segs[d]; s < doc_segs[d + 1]; ++s) {
+            seg_doc[s] = static_cast<uint32_t>(d);
+            uint64_t len = seg_off[s + 1] - seg_off[s];
+            uint64_t W = len >= q ? len - q + 1 : 0;
+            seg_wbase[s + 1] = seg_wbase[s] + W;
+            doc_w[d] += W;
+        }
+        if (seg_off[doc_segs[d + 1]] - doc_start[d] >= 0xffffffffull)
+            throw UsageError("build: documents larger than 4 GiB are not supported");
+    }
+    const uint64_t total_bytes = n_segs ? seg_off[n_segs] : 0;
+    const uint64_t total_w = seg_wbase[n_segs];
+
+    DevBuf d_seqs, d_segoff, d_segw, d_segdoc, d_docstart, d_tab, d_taboff, d_tabslots, d_tc;
+    d_seqs.reserve(std::max<uint64_t>(total_bytes, 1));
+    d_segoff.reserve(8 * (n_segs + 1));
+    d_segw.reserve(8 * (n_segs + 1));
+    d_segdoc.reserve(4 * std::max<uint64_t>(n_segs, 1));
+    d_docstart.reserve(8 * n_docs);
+    d_tc.reserve(8 * n_docs);
+    auto t_h2d = std::chrono::steady_clock::now();
+    COBS_CUDA(cudaMemcpyAsync(d_seqs.ptr, seqs, total_bytes, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_segoff.ptr, seg_off, 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_wbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
+    if (n_segs)
+        COBS_CUDA(cudaMemcpyAsync(d_segdoc.ptr, seg_doc.data(), 4 * n_segs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_docstart.ptr, doc_start.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemsetAsync(d_tc.ptr, 0, 8 * n_docs, st));
+    COBS_CUDA(cudaStreamSynchronize(st));
+    g_timing.ms_h2d = ms_since(t_h2d);
+
+    WinArgs wa{};
+    wa.seqs = d_seqs.as<uint8_t>();
+    wa.seg_off = d_segoff.as<uint64_t>();
+    wa.seg_wbase = d_segw.as<uint64_t>();
+    wa.seg_doc = d_segdoc.as<uint32_t>();
+    wa.doc_start = d_docstart.as<uint64_t>();
+    wa.q = q;
+    wa.k = P.k;
+    wa.canonical = P.canonical ? 1 : 0;
+
+    cudaEvent_t e0, e1, e2, e3;
+    COBS_CUDA(cudaEventCreate(&e0));
+    COBS_CUDA(cudaEventCreate(&e1));
+    COBS_CUDA(cudaEventCreate(&e2));
+    COBS_CUDA(cudaEventCreate(&e3));
+
+    // ---- count pass, in document chunks bounded by set memory ----------
+    std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
+    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(2 * doc_w[d]);
+    size_t free_b = 0, total_b = 0;
+    COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t budget_slots = std::max<uint64_t>((free_b / 3) / 8, 1ull << 20);
+    d_taboff.reserve(8 * n_docs);
+    d_tabslots.reserve(8 * n_docs);
+    COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+    float ms_count = 0;
+    for (uint64_t d0 = 0; d0 < n_docs;) {
+        uint64_t d1 = d0, slots = 0;
+        while (d1 < n_docs && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
+            tab_off[d1] = slots;
+            slots += tab_slots[d1];
+            ++d1;
+        }
+        d_tab.reserve(8 * slots);
+        COBS_CUDA(cudaMemcpyAsync(d_taboff.as<uint64_t>() + d0, tab_off.data() + d0, 8 * (d1 - d0),
+                                  cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaEventRecord(e0, st));
+        COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
+        wa.seg_lo = doc_segs[d0];
+        wa.seg_hi = doc_segs[d1];
+        wa.w_lo = seg_wbase[wa.seg_lo];
+        wa.w_hi = seg_wbase[wa.seg_hi];
+        if (wa.w_hi > wa.w_lo) {
+            // tab_off of the chunk's documents is relative to the chunk's tables
+            count_kernel<<<148 * 8, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(),
+                                                  d_taboff.as<uint64_t>(), d_tabslots.as<uint64_t>(),
+                                                  d_tc.as<unsigned long long>());
+            COBS_CUDA(cudaGetLastError());
+        }
+        COBS_CUDA(cudaEventRecord(e1, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        float t = 0;
+        cudaEventElapsedTime(&t, e0, e1);
+        ms_count += t;
+        d0 = d1;
+    }
+    g_timing.ms_count = ms_count;
+    std::vector<uint64_t> tc(n_docs);
+    COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
+    d_tab = DevBuf();
+
+    // ---- host: order, blocks, widths ------------------------------------
+    IndexMeta meta;
+    meta.params = P;
+    meta.kind = kind;
+    std::vector<uint64_t> order(n_docs);
+    std::iota(order.begin(), order.end(), 0);
+    uint64_t B = n_docs;
+    if (kind == kKindCompact) {
+        std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { // compact_index.cpp:27-30
+            if (tc[a] != tc[b]) return tc[a] < tc[b];
+            return names[a] < names[b];
+        });
+        B = P.block_size;
+    }
+    const uint64_t nb = (n_docs + B - 1) / B;
+    std::vector<uint32_t> doc_block(n_docs), doc_col(n_docs);
+    for (uint64_t b = 0; b < nb; ++b) {
+        uint64_t lo = b * B, hi = std::min(n_docs, lo + B), mx = 0;
+        BlockMeta bm;
+        bm.doc_count = hi - lo;
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint64_t d = order[i];
+            meta.docs.push_back({names[d], tc[d]});
+            mx = std::max(mx, tc[d]);
+            doc_block[d] = static_cast<uint32_t>(b);
+            doc_col[d] = static_cast<uint32_t>(i - lo);
+        }
+        bm.w = (kind == kKindClassic && forced_w != 0) ? forced_w : bloom::size_filter(mx, P.p, P.k);
+        meta.blocks.push_back(bm);
+    }
+    meta.layout();
+    std::vector<uint8_t> header = meta.header_bytes(); // throws on > 65535-byte names
+    const uint64_t payload = meta.file_size - meta.payload_start;
+
+    // ---- fill pass ------------------------------------------------------
+    std::vector<FillBlock> fb(nb);
+    for (uint64_t b = 0; b < nb; ++b) {
+        fb[b].base = meta.blocks[b].offset - meta.payload_start;
+        fb[b].w = meta.blocks[b].w;
+        fb[b].magic = mod_magic(meta.blocks[b].w);
+        fb[b].rb = meta.blocks[b].row_bytes();
+    }
+    DevBuf d_fb, d_dblock, d_dcol, d_words;
+    d_fb.reserve(sizeof(FillBlock) * nb);
+    d_dblock.reserve(4 * n_docs);
+    d_dcol.reserve(4 * n_docs);
+    size_t free2 = 0;
+    COBS_CUDA(cudaMemGetInfo(&free2, &total_b));
+    if ((payload + 3) / 4 * 4 + (64ull << 20) > free2)
+        throw DataError("index matrix (" + std::to_string(payload) +
+                        " bytes) does not fit in free device memory");
+    d_words.reserve(std::max<uint64_t>((payload + 3) / 4 * 4, 4));
+    COBS_CUDA(cudaMemcpyAsync(d_fb.ptr, fb.data(), sizeof(FillBlock) * nb, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_dblock.ptr, doc_block.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_dcol.ptr, doc_col.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaEventRecord(e2, st));
+    COBS_CUDA(cudaMemsetAsync(d_words.ptr, 0, (payload + 3) / 4 * 4, st));
+    wa.seg_lo = 0;
+    wa.seg_hi = n_segs;
+    wa.w_lo = 0;
+    wa.w_hi = total_w;
+    if (total_w > 0) {
+        fill_kernel<<<148 * 16, 256, 0, st>>>(wa, d_fb.as<FillBlock>(), d_dblock.as<uint32_t>(),
+                                              d_dcol.as<uint32_t>(), d_words.as<unsigned int>());
+        COBS_CUDA(cudaGetLastError());
+    }
+    COBS_CUDA(cudaEventRecord(e3, st));
+    COBS_CUDA(cudaStreamSynchronize(st));
+    float ms_fill = 0;
+    cudaEventElapsedTime(&ms_fill, e2, e3);
+    g_timing.ms_fill = ms_fill;
+
+    std::vector<uint8_t> image(header.size() + payload);
+    std::memcpy(image.data(), header.data(), header.size());
+    auto t_d2h = std::chrono::steady_clock::now();
+    if (payload)
+        COBS_CUDA(cudaMemcpy(image.data() + header.size(), d_words.ptr, payload, cudaMemcpyDeviceToHost));
+    g_timing.ms_d2h = ms_since(t_d2h);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    g_timing.ms_total = ms_since(t_start);
+    return image;
+}
+
+void write_image(const std::vector<uint8_t>& image, const std::string& path) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc); // storage.cpp:382-396
+    if (!out) throw DataError("cannot create index file: " + path);
+    out.write(reinterpret_cast<const char*>(image.data()), static_cast<std::streamsize>(image.size()));
+    out.flush();
+    if (!out) throw DataError("error writing index file: " + path);
+}
+
+// ---- synthetic documents on the device ---------------------------------
+
+__global__ void synth_docs_kernel(uint64_t seed, int alpha, const uint64_t* doc_off, uint64_t doc_lo,
+                                  uint64_t n_docs, uint64_t total, uint8_t* out) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = n_docs; // doc_off[lo] <= g < doc_off[hi]
+        while (hi - lo > 1) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (doc_off[mid] <= g)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        out[g] = static_cast<uint8_t>(
+            syn_sym_char(alpha, syn_doc_sym(seed, alpha, doc_lo + lo, g - doc_off[lo])));
+    }
+}
+
+void synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo, uint64_t doc_hi,
+                uint8_t* dev_out, int device) {
+    COBS_CUDA(cudaSetDevice(device));
+    uint64_t n = doc_hi - doc_lo;
+    std::vector<uint64_t> off(n + 1, 0);
+    for (uint64_t i = 0; i < n; ++i) off[i + 1] = off[i] + doc_len[doc_lo + i];
+    DevBuf d_off;
+    d_off.reserve(8 * (n + 1));
+    COBS_CUDA(cudaMemcpy(d_off.ptr, off.data(), 8 * (n + 1), cudaMemcpyHostToDevice));
+    if (off[n] > 0) synth_docs_kernel<<<148 * 16, 256>>>(seed, alpha, d_off.as<uint64_t>(), doc_lo, n, off[n], dev_out);
+    COBS_CUDA(cudaGetLastError());
+    COBS_CUDA(cudaDeviceSynchronize());
+}
+
+} // namespace cobsg

@@ -1,0 +1,26 @@
+// Kernel 4 driver: device index construction (see build.cu).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+namespace cobsg {
+
+struct BuildTiming {
+    double ms_h2d = 0, ms_count = 0, ms_fill = 0, ms_d2h = 0, ms_total = 0;
+};
+const BuildTiming& last_build_timing();
+
+// extract_terms + build_classic / build_compact + the writer's byte layout:
+// returns the complete file image.
+std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, uint64_t n_segs,
+                                 const uint64_t* doc_segs, const std::vector<std::string>& names,
+                                 const Params& params, uint8_t kind, uint64_t forced_w, int device);
+void write_image(const std::vector<uint8_t>& image, const std::string& path);
+
+void synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo, uint64_t doc_hi,
+                uint8_t* dev_out, int device);
+
+} // namespace cobsg

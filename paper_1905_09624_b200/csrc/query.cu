@@ -1,0 +1,650 @@
+// The COBS query hot path on sm_100a: three kernels behind one batch call.
+//
+//   kernel 1  termize_hash_kernel   windows -> canonical terms -> XXH64 ->
+//             exact per-query dedup (lock-free set) -> seed-major hashes, l,
+//             skipped, tau.            (reference: query.cpp:127-146,
+//             termizer.cpp:103-129, xxhash64.hpp:45-95, bloom.cpp:120-123)
+//   kernel 2  gather_kernel         one warp per (query, block, 1024-document
+//             slice): stream the k rows of every term (128-byte coalesced
+//             loads), AND them, add the 32-bit document masks into bit-sliced
+//             counters with a carry-save (Harley-Seal) adder, then threshold
+//             and compact hits; optional dense scores.
+//                                      (reference: query.cpp:49-119)
+//   kernel 3  ordering              CUB radix sorts on (query, score desc,
+//             name rank asc) (reference: query.cpp:156-162).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cub/cub.cuh>
+
+#include "../../include/cobs_gpu.h"
+#include "index.hpp"
+
+namespace cobsg {
+
+namespace {
+
+constexpr int kTermizeThreads = 256;
+constexpr uint32_t kSmemSlots = 8192; // 64 KB of shared set per CTA
+constexpr uint64_t kNoGtab = ~0ull;
+
+inline uint64_t next_pow2(uint64_t x) {
+    uint64_t p = 2;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+__device__ __forceinline__ uint64_t next_pow2_dev(uint64_t x) {
+    uint64_t p = 2;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// ---- kernel 1 -----------------------------------------------------------
+
+struct TermizeArgs {
+    const uint8_t* pats;
+    const uint64_t* off;
+    const uint64_t* win_base; // n+1 prefix of windows
+    const uint64_t* tab_off;  // per query: slot offset into gtab, or kNoGtab
+    unsigned long long* gtab;
+    uint64_t n;
+    uint32_t q, k;
+    int canonical;
+    double K;
+    uint64_t* hashes; // [win_total * k]
+    uint32_t* ell;
+    uint64_t* skipped;
+    uint32_t* tau;
+};
+
+__global__ void __launch_bounds__(kTermizeThreads) termize_hash_kernel(TermizeArgs a) {
+    extern __shared__ unsigned long long s_tab[];
+    using Scan = cub::BlockScan<uint32_t, kTermizeThreads>;
+    using Reduce = cub::BlockReduce<uint64_t, kTermizeThreads>;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Reduce::TempStorage reduce;
+    } tmp;
+    const uint32_t q = a.q, k = a.k;
+    for (uint64_t qi = blockIdx.x; qi < a.n; qi += gridDim.x) {
+        const uint64_t W = a.win_base[qi + 1] - a.win_base[qi];
+        const uint8_t* pat = a.pats + a.off[qi];
+        const uint64_t S = next_pow2_dev(2 * W);
+        unsigned long long* tab = a.tab_off[qi] == kNoGtab ? s_tab : a.gtab + a.tab_off[qi];
+        for (uint64_t s = threadIdx.x; s < S; s += blockDim.x) tab[s] = 0ull;
+        __syncthreads();
+        uint64_t* out = a.hashes + a.win_base[qi] * k;
+        uint64_t ell = 0, skipped = 0;
+        for (uint64_t base = 0; base < W; base += blockDim.x) {
+            uint64_t j = base + threadIdx.x;
+            uint32_t rep = 0;
+            uint64_t h0 = 0;
+            bool rc = false;
+            if (j < W) {
+                const uint8_t* w = pat + j;
+                bool valid = true;
+                if (a.canonical) { // termizer.cpp:112-119
+                    valid = window_acgt(w, q);
+                    if (valid) rc = choose_rc(w, q);
+                }
+                if (!valid) {
+                    ++skipped;
+                } else {
+                    h0 = xxh64_term(w, q, rc, 0);
+                    rep = set_insert(tab, S - 1, h0, static_cast<uint32_t>(j), pat, q,
+                                     a.canonical != 0, rc)
+                              ? 1u
+                              : 0u;
+                }
+            }
+            uint32_t excl, total;
+            Scan(tmp.scan).ExclusiveSum(rep, excl, total);
+            if (rep) { // seed-major per term: query.cpp:141-144
+                uint64_t* dst = out + (ell + excl) * k;
+                dst[0] = h0;
+                for (uint32_t s = 1; s < k; ++s) dst[s] = xxh64_term(pat + j, q, rc, s);
+            }
+            ell += total;
+            __syncthreads();
+        }
+        uint64_t skip_total = Reduce(tmp.reduce).Sum(skipped);
+        if (threadIdx.x == 0) {
+            a.ell[qi] = static_cast<uint32_t>(ell);
+            a.skipped[qi] = skip_total;
+            // bloom.cpp:120-123 with the host's separate roundings (no FMA)
+            double t = ceil(__dsub_rn(__dmul_rn(a.K, (double)ell), 1e-9));
+            uint64_t tau = t < 1.0 ? 1 : static_cast<uint64_t>(t);
+            a.tau[qi] = ell ? static_cast<uint32_t>(tau) : 0u;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- kernel 2 -----------------------------------------------------------
+
+struct GatherArgs {
+    const uint8_t* payload;
+    const DevBlock* blocks;
+    const uint32_t* ct; // (block, slice) pairs
+    uint32_t nct;
+    const uint64_t* hashes;
+    const uint64_t* win_base;
+    const uint32_t* ell;
+    const uint32_t* tau;
+    uint64_t n;
+    uint32_t k;
+    uint32_t qt; // queries per tile (multiple of 8)
+    uint64_t D;
+    void* scores; // dense [n][D] (uint16 or uint32) or null
+    int want_hits;
+    uint32_t* hit_count; // per query
+    unsigned long long* hit_total;
+    uint64_t hit_cap;
+    uint32_t* hit_q;
+    uint32_t* hit_doc;
+    uint32_t* hit_score;
+};
+
+// Carry-save adder: (hi, lo) = a + b + c.
+__device__ __forceinline__ void csa(uint32_t& hi, uint32_t& lo, uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t u = a ^ b;
+    hi = (a & b) | (u & c);
+    lo = u ^ c;
+}
+
+template <bool EF>
+__device__ __forceinline__ uint32_t ld_row(const uint8_t* p, uint64_t policy) {
+    uint32_t v;
+    if (EF)
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+            : "=r"(v)
+            : "l"(p), "l"(policy));
+    else
+        asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Bit-sliced counters: a document's count is sum_p 2^p * bit(F[p]).
+template <int NT>
+__device__ __forceinline__ void add_at(uint32_t (&F)[NT], int level, uint32_t x) {
+#pragma unroll
+    for (int p = 0; p < NT; ++p) {
+        if (p >= level) {
+            uint32_t t = F[p] & x;
+            F[p] ^= x;
+            x = t;
+        }
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ uint32_t extract(const uint32_t (&F)[NT], int i) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int p = 0; p < NT; ++p) s |= ((F[p] >> i) & 1u) << p;
+    return s;
+}
+
+// NP: bit planes above the four carry-save levels (NT = NP+4 total; the
+// batch's max window count must be < 2^NT).  KT: k if 1, else 0 (runtime k).
+// EF: L2 evict-first row loads (index far larger than L2).
+template <int NP, int KT, bool EF>
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+    constexpr int NT = NP + 4;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t groups = (a.qt + 7) / 8;
+    const uint64_t per_tile = groups * a.nct;
+    const uint64_t bid = blockIdx.x;
+    const uint64_t tile = bid / per_tile;
+    const uint64_t r = bid - tile * per_tile;
+    const uint32_t cti = static_cast<uint32_t>(r / groups);
+    const uint64_t qg = r - static_cast<uint64_t>(cti) * groups;
+    const uint64_t qin = qg * 8 + warp;
+    const uint64_t qi = tile * a.qt + qin;
+    if (qin >= a.qt || qi >= a.n) return;
+    const uint32_t ell = a.ell[qi];
+    if (ell == 0) return; // DataError query: no scores, no hits
+    const uint32_t k = KT ? KT : a.k;
+    const DevBlock B = a.blocks[a.ct[2 * cti]];
+    const uint32_t slice = a.ct[2 * cti + 1];
+    const uint32_t lane_byte = slice * 128u + lane * 4u;
+    const bool lane_ok = lane_byte < B.pitch;
+    const uint8_t* rowbase = a.payload + B.base + lane_byte;
+    const uint64_t* hq = a.hashes + a.win_base[qi] * k;
+    uint64_t policy = 0;
+    if (EF) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
+    uint32_t P[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) P[p] = 0;
+
+    const uint32_t hl = lane & 15u;
+    for (uint32_t t0 = 0; t0 < ell; t0 += 16) {
+        const uint32_t tl = t0 + hl;
+        const bool tv = tl < ell;
+        uint32_t v[16];
+        {
+            uint64_t off = tv ? fastmod(__ldg(hq + (uint64_t)tl * k), B.w, B.magic) * B.pitch : 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                uint64_t o = __shfl_sync(0xffffffffu, off, u);
+                v[u] = (lane_ok && t0 + u < ell) ? ld_row<EF>(rowbase + o, policy) : 0u;
+            }
+        }
+        for (uint32_t s = 1; s < k; ++s) { // AND the k rows: query.cpp:65-73
+            uint64_t off =
+                tv ? fastmod(__ldg(hq + (uint64_t)tl * k + s), B.w, B.magic) * B.pitch : 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                uint64_t o = __shfl_sync(0xffffffffu, off, u);
+                v[u] &= (lane_ok && t0 + u < ell) ? ld_row<EF>(rowbase + o, policy) : 0u;
+            }
+        }
+        // Harley-Seal: 16 masks -> ones/twos/fours/eights + one weight-16 mask
+        uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+        csa(twosA, ones, ones, v[0], v[1]);
+        csa(twosB, ones, ones, v[2], v[3]);
+        csa(foursA, twos, twos, twosA, twosB);
+        csa(twosA, ones, ones, v[4], v[5]);
+        csa(twosB, ones, ones, v[6], v[7]);
+        csa(foursB, twos, twos, twosA, twosB);
+        csa(eightsA, fours, fours, foursA, foursB);
+        csa(twosA, ones, ones, v[8], v[9]);
+        csa(twosB, ones, ones, v[10], v[11]);
+        csa(foursA, twos, twos, twosA, twosB);
+        csa(twosA, ones, ones, v[12], v[13]);
+        csa(twosB, ones, ones, v[14], v[15]);
+        csa(foursB, twos, twos, twosA, twosB);
+        csa(eightsB, fours, fours, foursA, foursB);
+        csa(sixteens, eights, eights, eightsA, eightsB);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) { // ripple the weight-16 mask
+            uint32_t c = P[p] & sixteens;
+            P[p] ^= sixteens;
+            sixteens = c;
+        }
+    }
+    // Flush the carry-save state into plain bit planes F (weight 2^p).
+    uint32_t F[NT];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) F[p] = 0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) F[p + 4] = P[p];
+    add_at<NT>(F, 3, eights);
+    add_at<NT>(F, 2, fours);
+    add_at<NT>(F, 1, twos);
+    add_at<NT>(F, 0, ones);
+
+    // Documents d < dc only: padding columns never count (query.cpp:84-86).
+    const uint32_t d0 = slice * 1024u + lane * 32u;
+    uint32_t valid = 0;
+    if (d0 < B.dc) valid = (B.dc - d0 >= 32u) ? 0xffffffffu : ((1u << (B.dc - d0)) - 1u);
+    const uint64_t gdoc0 = static_cast<uint64_t>(B.doc_base) + d0;
+
+    if (a.scores) {
+        if (NT <= 16) {
+            uint16_t* row = static_cast<uint16_t*>(a.scores) + qi * a.D + gdoc0;
+            for (int i = 0; i < 32; ++i)
+                if ((valid >> i) & 1u) row[i] = static_cast<uint16_t>(extract<NT>(F, i));
+        } else {
+            uint32_t* row = static_cast<uint32_t*>(a.scores) + qi * a.D + gdoc0;
+            for (int i = 0; i < 32; ++i)
+                if ((valid >> i) & 1u) row[i] = extract<NT>(F, i);
+        }
+    }
+    if (!a.want_hits) return;
+    // Bit-sliced F >= tau over all 32 documents of the lane at once.
+    const uint32_t tau = a.tau[qi];
+    uint32_t gt = 0, eq = 0xffffffffu;
+#pragma unroll
+    for (int p = NT - 1; p >= 0; --p) {
+        uint32_t tb = ((tau >> p) & 1u) ? 0xffffffffu : 0u;
+        gt |= eq & F[p] & ~tb;
+        eq &= ~(F[p] ^ tb);
+    }
+    if constexpr (NT < 32) {
+        if ((tau >> NT) != 0u) gt = eq = 0; // unreachable: tau <= l < 2^NT
+    }
+    uint32_t hits = (gt | eq) & valid;
+    uint32_t cnt = __popc(hits);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    unsigned long long base = 0;
+    if (lane == 31) {
+        base = atomicAdd(a.hit_total, (unsigned long long)total);
+        atomicAdd(a.hit_count + qi, total);
+    }
+    base = __shfl_sync(0xffffffffu, base, 31);
+    uint64_t idx = base + incl - cnt;
+    while (hits) {
+        int i = __ffs(hits) - 1;
+        hits &= hits - 1;
+        if (idx < a.hit_cap) {
+            a.hit_q[idx] = static_cast<uint32_t>(qi);
+            a.hit_doc[idx] = static_cast<uint32_t>(gdoc0 + i);
+            a.hit_score[idx] = extract<NT>(F, i);
+        }
+        ++idx;
+    }
+}
+
+// ---- kernel 3 helpers ---------------------------------------------------
+
+__global__ void make_keys_kernel(uint64_t m, const uint32_t* score, const uint32_t* doc,
+                                 const uint32_t* rank, int rbits, uint32_t smask, uint64_t* key,
+                                 uint32_t* perm) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    // (score desc, name asc) as one ascending key
+    key[i] = (static_cast<uint64_t>(~score[i] & smask) << rbits) | rank[doc[i]];
+    perm[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void gather_u32_kernel(uint64_t m, const uint32_t* perm, const uint32_t* src,
+                                  uint32_t* dst) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < m) dst[i] = src[perm[i]];
+}
+
+int bits_for(uint64_t v) { // bits to represent values 0..v
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return std::max(b, 1);
+}
+
+using GatherFn = void (*)(GatherArgs);
+
+template <int NP>
+GatherFn pick_k(uint32_t k, bool ef) {
+    if (k == 1) return ef ? gather_kernel<NP, 1, true> : gather_kernel<NP, 1, false>;
+    return ef ? gather_kernel<NP, 0, true> : gather_kernel<NP, 0, false>;
+}
+
+GatherFn pick_gather(int nt_needed, uint32_t k, bool ef) {
+    if (nt_needed <= 8) return pick_k<4>(k, ef);
+    if (nt_needed <= 12) return pick_k<8>(k, ef);
+    if (nt_needed <= 16) return pick_k<12>(k, ef);
+    return pick_k<28>(k, ef);
+}
+
+} // namespace
+
+void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offsets, uint64_t n,
+                 double K, uint64_t top_t, uint32_t flags, QueryResults& R) {
+    if (!(K > 0.0 && K <= 1.0)) throw UsageError("query: K must be in (0,1]"); // query.cpp:125
+    std::lock_guard<std::mutex> lock(ix.mu);
+    COBS_CUDA(cudaSetDevice(ix.device));
+    QueryWorkspace& ws = ix.ws;
+    cudaStream_t st = ix.stream;
+    const Params& P = ix.meta.params;
+    const uint32_t q = P.q, k = P.k;
+    const uint64_t D = ix.meta.total_docs();
+    const bool dev_in = flags & COBS_Q_DEVICE_INPUT;
+    R = QueryResults();
+    R.n = n;
+    if (n == 0) return;
+
+    // Host-side window accounting (needs the offsets on the host).
+    std::vector<uint64_t> h_off(n + 1);
+    if (dev_in)
+        COBS_CUDA(cudaMemcpy(h_off.data(), offsets, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    else
+        std::copy(offsets, offsets + n + 1, h_off.begin());
+    std::vector<uint64_t> win_base(n + 1), tab_off(n);
+    uint64_t wmax = 0, gslots = 0;
+    win_base[0] = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t len = h_off[i + 1] - h_off[i];
+        uint64_t W = len >= q ? len - q + 1 : 0; // termizer.cpp:109-110
+        if (W >= 0xffffffffull) throw UsageError("query: pattern longer than 2^32-2 grams");
+        win_base[i + 1] = win_base[i] + W;
+        wmax = std::max(wmax, W);
+        uint64_t S = next_pow2(2 * W);
+        if (S <= kSmemSlots) {
+            tab_off[i] = kNoGtab;
+        } else {
+            tab_off[i] = gslots;
+            gslots += S;
+        }
+    }
+    const uint64_t wtot = win_base[n];
+    const uint64_t pat_bytes = h_off[n] - h_off[0];
+
+    cudaEvent_t ev_begin, ev_end;
+    COBS_CUDA(cudaEventCreate(&ev_begin));
+    COBS_CUDA(cudaEventCreate(&ev_end));
+    COBS_CUDA(cudaEventRecord(ev_begin, st));
+
+    // Buffers
+    const uint8_t* d_pats;
+    const uint64_t* d_off;
+    if (dev_in) {
+        d_pats = patterns;
+        d_off = offsets;
+    } else {
+        ws.pats.reserve(std::max<uint64_t>(h_off[n], 1));
+        ws.offs.reserve(sizeof(uint64_t) * (n + 1));
+        COBS_CUDA(cudaMemcpyAsync(ws.pats.ptr, patterns, h_off[n], cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(ws.offs.ptr, offsets, sizeof(uint64_t) * (n + 1),
+                                  cudaMemcpyHostToDevice, st));
+        d_pats = ws.pats.as<uint8_t>();
+        d_off = ws.offs.as<uint64_t>();
+    }
+    (void)pat_bytes;
+    ws.win_base.reserve(sizeof(uint64_t) * (n + 1));
+    ws.tab_off.reserve(sizeof(uint64_t) * n);
+    ws.gtab.reserve(std::max<uint64_t>(gslots, 1) * 8);
+    ws.hashes.reserve(std::max<uint64_t>(wtot * k, 1) * 8);
+    ws.ell.reserve(4 * n);
+    ws.skipped.reserve(8 * n);
+    ws.tau.reserve(4 * n);
+    ws.hit_count.reserve(4 * n);
+    ws.hit_total.reserve(8);
+    COBS_CUDA(cudaMemcpyAsync(ws.win_base.ptr, win_base.data(), 8 * (n + 1), cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(ws.tab_off.ptr, tab_off.data(), 8 * n, cudaMemcpyHostToDevice, st));
+
+    cudaEvent_t ev[4];
+    for (auto& e : ev) COBS_CUDA(cudaEventCreate(&e));
+    COBS_CUDA(cudaEventRecord(ev[0], st));
+
+    // kernel 1
+    TermizeArgs ta{};
+    ta.pats = d_pats;
+    ta.off = d_off;
+    ta.win_base = ws.win_base.as<uint64_t>();
+    ta.tab_off = ws.tab_off.as<uint64_t>();
+    ta.gtab = ws.gtab.as<unsigned long long>();
+    ta.n = n;
+    ta.q = q;
+    ta.k = k;
+    ta.canonical = P.canonical ? 1 : 0;
+    ta.K = K;
+    ta.hashes = ws.hashes.as<uint64_t>();
+    ta.ell = ws.ell.as<uint32_t>();
+    ta.skipped = ws.skipped.as<uint64_t>();
+    ta.tau = ws.tau.as<uint32_t>();
+    uint64_t small_S = 2;
+    for (uint64_t i = 0; i < n; ++i)
+        if (tab_off[i] == kNoGtab) small_S = std::max(small_S, next_pow2(2 * (win_base[i + 1] - win_base[i])));
+    size_t smem = static_cast<size_t>(std::min<uint64_t>(small_S, kSmemSlots)) * 8;
+    COBS_CUDA(cudaFuncSetAttribute(termize_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    unsigned grid1 = static_cast<unsigned>(std::min<uint64_t>(n, 1u << 30));
+    termize_hash_kernel<<<grid1, kTermizeThreads, smem, st>>>(ta);
+    COBS_CUDA(cudaGetLastError());
+    R.launches += 1;
+    COBS_CUDA(cudaEventRecord(ev[1], st));
+
+    // kernel 2
+    const bool want_scores = flags & COBS_Q_SCORES;
+    const bool want_hits = (flags & COBS_Q_HITS) || !(flags & COBS_Q_SCORES);
+    int nt_needed = bits_for(wmax);
+    R.score_bytes = nt_needed <= 16 ? 2 : 4;
+    if (want_scores) {
+        ws.scores.reserve(std::max<uint64_t>(n * D * R.score_bytes, 1));
+        COBS_CUDA(cudaMemsetAsync(ws.scores.ptr, 0, n * D * R.score_bytes, st));
+    }
+    if (ws.hit_cap == 0) {
+        ws.hit_cap = 1u << 20;
+        ws.hit_q.reserve(4 * ws.hit_cap);
+        ws.hit_doc.reserve(4 * ws.hit_cap);
+        ws.hit_score.reserve(4 * ws.hit_cap);
+    }
+    GatherArgs ga{};
+    ga.payload = ix.payload;
+    ga.blocks = ix.d_blocks;
+    ga.ct = ix.d_ct;
+    ga.nct = static_cast<uint32_t>(ix.ct_block.size());
+    ga.hashes = ws.hashes.as<uint64_t>();
+    ga.win_base = ws.win_base.as<uint64_t>();
+    ga.ell = ws.ell.as<uint32_t>();
+    ga.tau = ws.tau.as<uint32_t>();
+    ga.n = n;
+    ga.k = k;
+    uint64_t qt = 2048;
+    if (const char* e = std::getenv("COBS_QT")) qt = std::max<uint64_t>(8, std::strtoull(e, nullptr, 10));
+    qt = std::min<uint64_t>((qt + 7) / 8 * 8, (n + 7) / 8 * 8);
+    ga.qt = static_cast<uint32_t>(qt);
+    ga.D = D;
+    ga.scores = want_scores ? ws.scores.ptr : nullptr;
+    ga.want_hits = want_hits ? 1 : 0;
+    ga.hit_count = ws.hit_count.as<uint32_t>();
+    ga.hit_total = ws.hit_total.as<unsigned long long>();
+    GatherFn fn = pick_gather(nt_needed, k, ix.evict_first);
+    const uint64_t tiles = (n + qt - 1) / qt;
+    const uint64_t grid2 = tiles * ((qt + 7) / 8) * ga.nct;
+    if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
+    unsigned long long h_total = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        ga.hit_cap = ws.hit_cap;
+        ga.hit_q = ws.hit_q.as<uint32_t>();
+        ga.hit_doc = ws.hit_doc.as<uint32_t>();
+        ga.hit_score = ws.hit_score.as<uint32_t>();
+        COBS_CUDA(cudaMemsetAsync(ws.hit_count.ptr, 0, 4 * n, st));
+        COBS_CUDA(cudaMemsetAsync(ws.hit_total.ptr, 0, 8, st));
+        if (attempt == 0) COBS_CUDA(cudaEventRecord(ev[1], st));
+        if (grid2 > 0) {
+            fn<<<static_cast<unsigned>(grid2), 256, 0, st>>>(ga);
+            R.launches += 1;
+        }
+        COBS_CUDA(cudaGetLastError());
+        COBS_CUDA(cudaEventRecord(ev[2], st));
+        COBS_CUDA(cudaMemcpyAsync(&h_total, ws.hit_total.ptr, 8, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        if (h_total <= ws.hit_cap) break;
+        ws.hit_cap = h_total + h_total / 8;
+        ws.hit_q.reserve(4 * ws.hit_cap);
+        ws.hit_doc.reserve(4 * ws.hit_cap);
+        ws.hit_score.reserve(4 * ws.hit_cap);
+    }
+
+    // kernel 3: order hits by (query, score desc, name asc)
+    const uint64_t m = h_total;
+    if (want_hits && m > 0) {
+        ws.key64.reserve(8 * m);
+        ws.key64_alt.reserve(8 * m);
+        ws.key32.reserve(4 * m);
+        ws.key32_alt.reserve(4 * m);
+        ws.perm.reserve(4 * m);
+        ws.perm_alt.reserve(4 * m);
+        ws.out_doc.reserve(4 * m);
+        ws.out_score.reserve(4 * m);
+        int rbits = bits_for(D ? D - 1 : 0);
+        int sbits = nt_needed;
+        uint32_t smask = sbits >= 32 ? 0xffffffffu : ((1u << sbits) - 1u);
+        unsigned g = static_cast<unsigned>((m + 255) / 256);
+        make_keys_kernel<<<g, 256, 0, st>>>(m, ws.hit_score.as<uint32_t>(), ws.hit_doc.as<uint32_t>(),
+                                            ix.d_name_rank, rbits, smask, ws.key64.as<uint64_t>(),
+                                            ws.perm.as<uint32_t>());
+        COBS_CUDA(cudaGetLastError());
+        cub::DoubleBuffer<uint64_t> k64(ws.key64.as<uint64_t>(), ws.key64_alt.as<uint64_t>());
+        cub::DoubleBuffer<uint32_t> pv(ws.perm.as<uint32_t>(), ws.perm_alt.as<uint32_t>());
+        size_t tmp1 = 0, tmp2 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp1, k64, pv, static_cast<int>(m), 0, rbits + sbits, st);
+        cub::DoubleBuffer<uint32_t> k32(ws.key32.as<uint32_t>(), ws.key32_alt.as<uint32_t>());
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp2, k32, pv, static_cast<int>(m), 0, bits_for(n), st);
+        ws.cub_tmp.reserve(std::max(tmp1, tmp2));
+        tmp1 = ws.cub_tmp.bytes;
+        COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp1, k64, pv, static_cast<int>(m), 0,
+                                                  rbits + sbits, st));
+        // stable secondary sort by query id
+        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_q.as<uint32_t>(), k32.Current());
+        tmp2 = ws.cub_tmp.bytes;
+        COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp2, k32, pv, static_cast<int>(m), 0,
+                                                  bits_for(n), st));
+        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_doc.as<uint32_t>(),
+                                             ws.out_doc.as<uint32_t>());
+        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_score.as<uint32_t>(),
+                                             ws.out_score.as<uint32_t>());
+        COBS_CUDA(cudaGetLastError());
+        R.launches += 4;
+    }
+    COBS_CUDA(cudaEventRecord(ev[3], st));
+
+    // D2H: per-query metadata always (small); hits and scores unless the
+    // caller keeps results on the device.
+    const bool keep = flags & COBS_Q_KEEP_DEVICE;
+    R.ell.resize(n);
+    R.tau.resize(n);
+    R.skipped.resize(n);
+    std::vector<uint32_t> cnt(n);
+    COBS_CUDA(cudaMemcpyAsync(R.ell.data(), ws.ell.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+    COBS_CUDA(cudaMemcpyAsync(R.tau.data(), ws.tau.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+    COBS_CUDA(cudaMemcpyAsync(R.skipped.data(), ws.skipped.ptr, 8 * n, cudaMemcpyDeviceToHost, st));
+    COBS_CUDA(cudaMemcpyAsync(cnt.data(), ws.hit_count.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (!keep && want_hits && m > 0) {
+        R.doc.resize(m);
+        R.score.resize(m);
+        COBS_CUDA(cudaMemcpyAsync(R.doc.data(), ws.out_doc.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaMemcpyAsync(R.score.data(), ws.out_score.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
+    }
+    if (!keep && want_scores) {
+        R.scores.resize(n * D * R.score_bytes);
+        COBS_CUDA(cudaMemcpyAsync(R.scores.data(), ws.scores.ptr, R.scores.size(),
+                                  cudaMemcpyDeviceToHost, st));
+    }
+    COBS_CUDA(cudaEventRecord(ev_end, st));
+    COBS_CUDA(cudaStreamSynchronize(st));
+    R.status.assign(n, 0);
+    R.message.assign(n, std::string());
+    R.hit_off.resize(n);
+    R.hit_n.resize(n);
+    uint64_t o = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        R.hit_off[i] = o;
+        uint64_t c = want_hits ? cnt[i] : 0;
+        R.hit_n[i] = keep ? 0 : ((top_t > 0 && c > top_t) ? top_t : c); // query.cpp:161-162
+        o += c;
+        if (R.ell[i] == 0) { // query.cpp:133-138
+            R.status[i] = COBS_EDATA;
+            R.message[i] = R.skipped[i] > 0
+                               ? "query: all " + std::to_string(R.skipped[i]) +
+                                     " pattern grams were skipped by canonicalization"
+                               : "query: pattern shorter than q = " + std::to_string(q);
+        }
+        R.row_bytes += static_cast<uint64_t>(k) * R.ell[i] * ix.sum_row_bytes;
+    }
+    float t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    R.ms_termize = t01;
+    R.ms_gather = t12;
+    R.ms_order = t23;
+    float ttot = 0;
+    cudaEventElapsedTime(&ttot, ev_begin, ev_end);
+    R.ms_total = ttot;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(ev_begin);
+    cudaEventDestroy(ev_end);
+}
+
+} // namespace cobsg

@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+fixtures and the CPU oracle.  Bit-exact: hit lists, dense scores, l,
+skipped, error messages, built files."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_1905_09624_b200 as cb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GDIR = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rand(rng, n, alphabet=b"ACGT"):
+    return bytes(rng.choice(alphabet) for _ in range(n))
+
+
+def gpu_hits(view, b, i):
+    d, s = b.hits(i)
+    return [[int(x), int(y)] for x, y in zip(d, s)]
+
+
+def test_golden_fixtures(gpu):
+    g = json.load(open(os.path.join(GDIR, "golden.json")))
+    for name, spec in g["files"].items():
+        path = os.path.join(GDIR, name + ".cobs")
+        view = cb.open_resident(path, gpu)
+        res = g["results"][name]
+        # batch every (pattern, K, top_t) group through one call per (K, top_t)
+        groups = {}
+        for r in res:
+            groups.setdefault((r["K"], r["top_t"]), []).append(r)
+        for (K, top_t), rs in groups.items():
+            b = cb.query_batch(view, [r["pat"].encode() for r in rs], K, top_t)
+            for i, r in enumerate(rs):
+                if "error" in r:
+                    assert b.status[i] == r["error"] and b.messages[i] == r["msg"], (name, r)
+                else:
+                    assert b.status[i] == 0
+                    assert (int(b.ell[i]), int(b.skipped[i])) == (r["ell"], r["skipped"])
+                    assert gpu_hits(view, b, i) == r["hits"], (name, r["pat"], K, top_t)
+        # the GPU build reproduces the reference's file byte for byte
+        docs = [(d[0].encode(), [s.encode() for s in d[1]]) for d in spec["docs"]]
+        p = dict(spec["params"])
+        kind = p.pop("kind")
+        params = cb.IndexParams(**{k: v for k, v in p.items()})
+        assert cb.build_image(docs, params, kind, device=gpu) == open(path, "rb").read(), name
+        view.close()
+
+
+def test_query_api_mirror(gpu):
+    view = cb.open_resident(os.path.join(GDIR, "classic_k2.cobs"), gpu)
+    with pytest.raises(ValueError, match=r"query: K must be in \(0,1\]"):
+        cb.query(view, b"A" * 40, cb.QueryOptions(K=0.0))
+    with pytest.raises(ValueError):
+        cb.query(view, b"A" * 40, cb.QueryOptions(K=1.5))
+    with pytest.raises(cb.DataError, match="pattern shorter than q = 31"):
+        cb.query(view, b"ACGT")
+    r = cb.query(view, b"ACGT" * 20, cb.QueryOptions(K=1e-12))
+    assert r.ell > 0
+    assert view.params().k == 2 and view.kind() == cb.KIND_CLASSIC
+
+
+def corpus(rng, n, lo, hi, noisy=False, alphabet=b"ACGT"):
+    docs = []
+    for i in range(n):
+        a = alphabet + b"N" if noisy and i % 4 == 0 else alphabet
+        segs = [rand(rng, rng.randint(lo, hi), a) for _ in range(1 + (i % 3 == 0))]
+        if i % 7 == 6:
+            segs.append(b"")  # empty content string
+        docs.append((b"doc%04d" % i, segs))
+    return docs
+
+
+CASES = [
+    # (q, k, p, canonical, kind, block_size, alphabet)
+    (31, 1, 0.3, False, 0, 1024, b"ACGT"),
+    (31, 2, 0.3, True, 1, 4, b"ACGT"),
+    (31, 3, 0.3, False, 1, 3, b"ACGT"),
+    (10, 2, 0.1, False, 0, 1024, b"ACDEFGHIKLMNPQRSTVWY"),
+    (33, 1, 0.25, True, 1, 5, b"ACGT"),     # q >= 32: XXH64 stripe path
+    (5, 2, 0.3, False, 1, 2, b"ACGT"),      # tiny q: heavy duplication
+    (31, 1, 0.3, False, 1, 1, b"ACGT"),     # one document per block
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_random_corpora_scores_and_hits(gpu, case):
+    q, k, p, canonical, kind, B, alphabet = case
+    rng = random.Random(hash(case) & 0xFFFFFFF)
+    docs = corpus(rng, 37, 20, 3000, noisy=canonical, alphabet=alphabet)
+    img = O.build_image(docs, q=q, k=k, p=p, canonical=canonical, block_size=B, kind=kind)
+    params = cb.IndexParams(q=q, k=k, p=p, canonical=canonical, block_size=B)
+    assert cb.build_image(docs, params, kind, device=gpu) == img
+    idx = O.OracleIndex.parse(img)
+    view = cb.open_image(img, gpu)
+    pats = []
+    for i in range(40):
+        if i % 4 == 0:
+            pats.append(rand(rng, rng.randint(0, 400), alphabet))
+        else:
+            src = docs[i % len(docs)][1][0]
+            ln = min(len(src), rng.randint(q, 600))
+            st = rng.randrange(len(src) - ln + 1)
+            pat = bytearray(src[st:st + ln])
+            if i % 5 == 0 and len(pat) > 3:
+                pat[len(pat) // 2] = ord("N")
+            if i % 9 == 0:
+                pat = pat.lower()
+            pats.append(bytes(pat))
+    for K, top_t in [(1e-12, 0), (0.5, 0), (0.9, 3), (1.0, 0)]:
+        b = cb.query_batch(view, pats, K, top_t, scores=True)
+        for i, pat in enumerate(pats):
+            try:
+                ell, sk, hits, dense = idx.query(pat, K, top_t, scores=True)
+            except O.OracleError as e:
+                assert (b.status[i], b.messages[i]) == (e.code, e.msg)
+                continue
+            assert b.status[i] == 0
+            assert (int(b.ell[i]), int(b.skipped[i])) == (ell, sk)
+            assert gpu_hits(view, b, i) == [list(h) for h in hits]
+            assert np.array_equal(b.dense[i].astype(np.uint32), dense), (i, K)
+    view.close()
+
+
+def test_long_and_repetitive_patterns(gpu):
+    """Global-memory dedup sets (> 4096 windows), heavy duplication, and the
+    uint32 counter path at l > 65535 (test_query.cpp:207-234)."""
+    rng = random.Random(29)
+    big = rand(rng, 70000)
+    docs = [(b"big", [big]), (b"small", [rand(rng, 500)]), (b"rep", [b"ACGT" * 3000])]
+    img = O.build_image(docs)
+    idx = O.OracleIndex.parse(img)
+    view = cb.open_image(img, gpu)
+    pats = [big, big[1000:41000], b"ACGT" * 5000, b"A" * 9000, rand(rng, 12000),
+            (b"ACGTTGCA" * 800)[:6000]]
+    b = cb.query_batch(view, pats, 1e-12, scores=True)
+    names = view.doc_names()
+    for i, pat in enumerate(pats):
+        ell, sk, hits, dense = idx.query(pat, 1e-12, scores=True)
+        assert int(b.ell[i]) == ell
+        assert np.array_equal(b.dense[i].astype(np.uint32), dense)
+        assert gpu_hits(view, b, i) == [list(h) for h in hits]
+    assert b.dense.dtype == np.uint32  # > 65535 windows in the batch
+    r = cb.query(view, big, cb.QueryOptions(K=1.0))
+    assert r.hits[0].doc_name == b"big" and r.hits[0].score == r.ell > 65535
+    b2 = cb.query_batch(view, [big[1000:41000]], 0.9)
+    ell, sk, hits, _ = idx.query(big[1000:41000], 0.9)
+    assert gpu_hits(view, b2, 0) == [list(h) for h in hits]
+    view.close()
+
+
+def test_write_index_roundtrip(gpu, tmp_path):
+    for name in ("classic_k2", "compact_canon", "compact_k3", "tiny"):
+        src = os.path.join(GDIR, name + ".cobs")
+        view = cb.open_resident(src, gpu)
+        out = str(tmp_path / (name + ".cobs"))
+        cb.write_index(view, out)
+        assert open(out, "rb").read() == open(src, "rb").read()
+        for b in range(view.block_count()):
+            idx = O.OracleIndex.parse(open(src, "rb").read())
+            rb = view.row_bytes(b)
+            blk = idx.blocks()[b]
+            assert view.doc_count(b) == blk[0] and view.width(b) == blk[1]
+            assert len(view.row_data(b, 0)) == rb
+        view.close()
+
+
+def test_build_errors(gpu):
+    with pytest.raises(cb.DataError, match="build: no documents"):
+        cb.build_compact([], device=gpu)
+    with pytest.raises(cb.DataError, match="duplicate document name: a"):
+        cb.build_classic([(b"a", [b"A" * 40]), (b"b", []), (b"a", [])], device=gpu)
+    # zero-term documents, forced width, multi-segment documents
+    docs = [(b"e", []), (b"s", [b"ACG"]), (b"m", [b"A" * 40, b"C" * 35, b""])]
+    for fw in (0, 7, 1):
+        assert cb.build_classic(docs, forced_w=fw, device=gpu) == O.build_image(docs, forced_w=fw)
+    assert cb.build_compact(docs, cb.IndexParams(block_size=2), device=gpu) == \
+        O.build_image(docs, block_size=2, kind=1)
+
+
+def test_c5_procedural_small(gpu):
+    """Config-5 generator: device rows == host rows; header == oracle's
+    (and hence the reference writer's, test_oracle_vs_ref.py); scores == the
+    oracle over the procedural view."""
+    from paper_1905_09624_b200 import synth
+    seed, n, B, med, sig, p = 7, 3000, 1024, 4000.0, 0.5, 0.3
+    view = cb.synth_c5(seed, n, B, med, sig, p, device=gpu)
+    orc = O.OracleIndex.c5(seed, n, B, med, sig, p)
+    assert [(view.doc_count(b), view.width(b)) for b in range(view.block_count())] == \
+        [(dc, w) for dc, w, _ in orc.blocks()]
+    assert view.doc_names() == orc.names()
+    tcs = orc.term_counts()
+    for b, (dc, w, base) in enumerate(orc.blocks()):
+        thr = synth.c5_thr16(w, max(tcs[base:base + dc]))
+        for r in (0, 1, w // 2, w - 1):
+            assert view.row_data(b, r) == synth.c5_row(seed, b, r, (dc + 7) // 8, thr, dc)
+    rng = random.Random(5)
+    pats = [rand(rng, 1000) for _ in range(8)]
+    bres = cb.query_batch(view, pats, 1e-12, scores=True)
+    for i, pat in enumerate(pats):
+        ell, sk, hits, dense = orc.query(pat, 1e-12, scores=True)
+        assert np.array_equal(bres.dense[i].astype(np.uint32), dense)
+        assert gpu_hits(view, bres, i) == [list(h) for h in hits]
+    view.close()
