@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""COBS query / build benchmark on B200 (see DESIGN.md §6 for the contract).
+
+Default workload: BASELINE.json config 5 -- the 100,000-document compact
+index (~100 GB, resident in HBM) queried with 100,000 random 1,000-bp
+queries at K = 0.8.  One step = one batch of the whole query set through
+kernels 1-3.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+                    [--config c5|c1] [--queries Q]
+
+Arms:
+  gpu (default)  value: inputs resident in HBM; e2e: the reference-facing
+                 C-ABI call with host (pinned) patterns, H2D + D2H inside the
+                 timed region.  Adds roofline, cpu_baseline, build.
+  reference      the reference's own CPU implementation (oracle/_ref: the
+                 unmodified /root/reference sources) on the host cores, on a
+                 bounded sample of the same workload.
+Multi-GPU: weak scaling -- every rank holds its own replica of the index and
+queries its own batch (no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "query q-grams/sec and row-gather HBM GB/s (fraction of peak); docs/sec index build"
+UNIT = "q-grams/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c1"])
+    ap.add_argument("--queries", type=int, default=0, help="override the batch size")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="queries in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-build", action="store_true")
+    ap.add_argument("--c5-median", type=float, default=0.0)
+    ap.add_argument("--c5-docs", type=int, default=0)
+    return ap.parse_args()
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM traffic of the gather kernel from the committed ncu
+    capture (profiles/), scaled per algorithmic byte, or None."""
+    path = os.path.join(ROOT, "profiles", "gather_ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        if d.get("workload") != workload:
+            return None
+        return d
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- helpers
+
+def c5_config(args):
+    from paper_1905_09624_b200 import synth
+    cfg = synth.CONFIGS["c5"]
+    if args.c5_median:
+        cfg = synth.replace(cfg, c5_median=args.c5_median)
+    if args.c5_docs:
+        cfg = synth.replace(cfg, n_docs=args.c5_docs)
+    if args.queries:
+        cfg = synth.replace(cfg, n_queries=args.queries)
+    return cfg
+
+
+def workload_name(cfg):
+    if cfg.name == "c5":
+        return (f"c5: compact {cfg.n_docs}-document index (log-normal term counts, median "
+                f"{cfg.c5_median:.3g}, sigma {cfg.c5_sigma}), {cfg.n_queries} random {cfg.qlen}-bp "
+                f"queries, K={cfg.K}")
+    return (f"{cfg.name}: {'classic' if cfg.kind == 0 else 'compact'} {cfg.n_docs} docs, "
+            f"{cfg.n_queries} x {cfg.qlen}-bp queries, K={cfg.K}")
+
+
+def rank_query_ids(cfg, rank):
+    return np.arange(rank * cfg.n_queries, (rank + 1) * cfg.n_queries, dtype=np.uint64)
+
+
+def build_c1_index(cfg, device):
+    """Config-1 index built on the device from the seeded corpus."""
+    import paper_1905_09624_b200 as cb
+    from paper_1905_09624_b200 import synth
+    buf, off = synth.docs(cfg)
+    names = synth.doc_names(cfg)
+    docs = [(names[i], [buf[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
+    img = cb.build_classic(docs, cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p), device=device)
+    return cb.open_image(img, device)
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """The reference's own CPU query path (oracle/_ref = unmodified
+    /root/reference sources), threaded over all host cores."""
+    from oracle import oracle as O
+    from paper_1905_09624_b200 import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    if args.config == "c5":
+        cfg = c5_config(args)
+        t0 = time.perf_counter()
+        ref = O.RefIndex.c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma,
+                            cfg.p, materialise=True, threads=cores)
+        setup_s = time.perf_counter() - t0
+        per_step = args.cpu_sample or 2 * cores
+        K = cfg.K
+    else:
+        cfg = synth.CONFIGS["c1"]
+        import tempfile
+        buf, off = synth.docs(cfg)
+        names = synth.doc_names(cfg)
+        docs = [(names[i], [buf[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
+        t0 = time.perf_counter()
+        tmp = tempfile.mkdtemp()
+        O.ref_build_write(docs, os.path.join(tmp, "c1.cobs"), q=cfg.q, k=cfg.k, p=cfg.p)
+        ref = O.RefIndex.open(os.path.join(tmp, "c1.cobs"))
+        setup_s = time.perf_counter() - t0
+        per_step = args.cpu_sample or cfg.n_queries
+        K = cfg.K
+    times, grams = [], []
+    for step in range(args.warmup + args.steps):
+        ids = (np.arange(per_step, dtype=np.uint64) + step * per_step) % cfg.n_queries
+        qb, qo = synth.queries(cfg, ids)
+        t = time.perf_counter()
+        ell, sk, st, nh, _ = ref.query_batch(qb, qo, K, threads=cores)
+        dt = time.perf_counter() - t
+        if step >= args.warmup:
+            times.append(dt)
+            grams.append(int(ell.sum()))
+    value = sum(grams) / sum(times)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u64",
+        "data": "synthetic (seeded)", "impl": "reference",
+        "config": {"workload": workload_name(cfg), "step": f"{per_step}-query bounded sample",
+                   "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{per_step} queries per step x {args.steps} steps, "
+                                   f"index load {setup_s:.1f}s excluded"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- gpu arm
+
+def cpu_baseline_c5(cfg, sample):
+    from oracle import oracle as O
+    from paper_1905_09624_b200 import synth
+    cores = os.cpu_count() or 1
+    ref = O.RefIndex.c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p,
+                        materialise=True, threads=cores)
+    qb, qo = synth.queries(cfg, np.arange(sample, dtype=np.uint64))
+    t = time.perf_counter()
+    ell, sk, st, nh, _ = ref.query_batch(qb, qo, cfg.K, threads=cores)
+    dt = time.perf_counter() - t
+    ref.close()
+    return {"value": float(ell.sum()) / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{sample} of the batch's queries (ids 0..{sample - 1}) through the "
+                      f"reference query() over an in-RAM copy of the same index, "
+                      f"{cores} threads, {dt:.1f}s"}
+
+
+def run_gpu(args):
+    import torch
+    import paper_1905_09624_b200 as cb
+    from paper_1905_09624_b200 import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.config == "c5":
+        cfg = c5_config(args)
+        t0 = time.perf_counter()
+        view = cb.synth_c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma,
+                           cfg.p, device=local)
+    else:
+        cfg = synth.CONFIGS["c1"]
+        if args.queries:
+            cfg = synth.replace(cfg, n_queries=args.queries)
+        t0 = time.perf_counter()
+        view = build_c1_index(cfg, local)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream(device=local)
+    view.set_stream(stream.cuda_stream)
+
+    ids = rank_query_ids(cfg, rank) if cfg.name == "c5" else np.arange(cfg.n_queries, dtype=np.uint64)
+    qb, qo = synth.queries(cfg, ids)
+    n = len(qo) - 1
+    h_pat = torch.from_numpy(qb).pin_memory()
+    h_off = torch.from_numpy(qo.view(np.int64)).pin_memory()
+    d_pat = h_pat.to(f"cuda:{local}")
+    d_off = h_off.to(f"cuda:{local}")
+    torch.cuda.synchronize()
+
+    def step_device():
+        return cb.query_batch_raw(view, d_pat.data_ptr(), (d_off.data_ptr(), n), cfg.K,
+                                  device_input=True, keep_device=True)
+
+    def step_e2e():
+        return cb.query_batch_raw(view, h_pat.numpy(), h_off.numpy().view(np.uint64), cfg.K)
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            outs = [fn() for _ in range(steps)]
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if dist:
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, outs
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_dev, outs = timed(step_device, args.steps, args.warmup)
+    ms_e2e, outs_e2e = timed(step_e2e, args.steps, 1)
+    clk = clocks.stop()
+
+    grams = int(outs[-1].ell.astype(np.uint64).sum())
+    total_grams = grams
+    if dist:
+        t = torch.tensor([grams], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t)
+        total_grams = int(t.item())
+    value = total_grams / (ms_dev / 1e3)
+    e2e_value = total_grams / (ms_e2e / 1e3)
+    last = outs_e2e[-1]
+    h2d = int(qb.nbytes + qo.nbytes)
+    d2h = int(n * (4 + 4 + 8 + 4) + last.docs.nbytes + last.scores.nbytes)
+
+    # roofline of the dominant kernel (gather): algorithmic bytes
+    # k * sum(l) * sum_b row_bytes_b per launch / its event-timed duration
+    gather_ms = statistics.mean(o.ms_gather for o in outs)
+    algo_bytes = outs[-1].row_bytes
+    achieved = algo_bytes / (gather_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    tr = ncu_traffic(cfg.name)
+    traffic = None
+    if tr and tr.get("algo_bytes"):
+        traffic = tr["dram_bytes"] / tr["algo_bytes"] * algo_bytes
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "kernel": "gather_kernel", "algo_bytes_per_launch": algo_bytes,
+                "gather_ms": gather_ms,
+                "share_of_step": gather_ms / ms_dev,
+                "termize_ms": statistics.mean(o.ms_termize for o in outs),
+                "order_ms": statistics.mean(o.ms_order for o in outs)}
+
+    index_bytes = view.device_bytes()
+    cpu_base = None
+    build = None
+    if rank == 0 and world == 1:
+        if not args.no_build:
+            build = bench_build(cb, synth, local)
+        if not args.no_cpu_baseline:
+            view.close()  # free nothing on host; the CPU leg allocates its own copy
+            try:
+                if cfg.name == "c5":
+                    cpu_base = cpu_baseline_c5(cfg, args.cpu_sample or 2000)
+                else:
+                    cpu_base = cpu_baseline_c1(cfg)
+            except Exception as e:  # report, do not die
+                cpu_base = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8/u64", "data": "synthetic (seeded)",
+            "config": {"workload": workload_name(cfg), "queries_per_gpu": n,
+                       "index_bytes_hbm": index_bytes,
+                       "l2": "inputs larger than L2 (index ~100 GB, hashes ~0.8 GB)"
+                             if cfg.name == "c5" else "index L2-resident (35 MB)",
+                       "parallelism": f"replicas x{world} (independent query batches)",
+                       "setup_s": setup_s},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+            "gpu_launches": int(sum(o.launches for o in outs)),
+            "roofline": roofline,
+            "cpu_baseline": cpu_base,
+            "build": build,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline_c1(cfg):
+    import tempfile
+    from oracle import oracle as O
+    from paper_1905_09624_b200 import synth
+    cores = os.cpu_count() or 1
+    buf, off = synth.docs(cfg)
+    names = synth.doc_names(cfg)
+    docs = [(names[i], [buf[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
+    tmp = tempfile.mkdtemp()
+    O.ref_build_write(docs, os.path.join(tmp, "c1.cobs"), q=cfg.q, k=cfg.k, p=cfg.p)
+    ref = O.RefIndex.open(os.path.join(tmp, "c1.cobs"))
+    qb, qo = synth.queries(cfg)
+    t = time.perf_counter()
+    ell, *_ = ref.query_batch(qb, qo, cfg.K, threads=cores)
+    dt = time.perf_counter() - t
+    return {"value": float(ell.sum()) / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"all {cfg.n_queries} queries, {cores} threads, {dt:.2f}s"}
+
+
+def bench_build(cb, synth, device):
+    """docs/s of index construction on the config-1 corpus (1,000 x 100 kb):
+    kernel time (sequences in HBM -> finished matrix) and end to end (host
+    sequences -> file image in host memory)."""
+    cfg = synth.CONFIGS["c1"]
+    buf, off = synth.docs(cfg)
+    names = synth.doc_names(cfg)
+    docs = [(names[i], [buf[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
+    params = cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p)
+    cb.build_classic(docs, params, device=device)  # warm-up
+    runs = []
+    for _ in range(3):
+        t = time.perf_counter()
+        cb.build_classic(docs, params, device=device)
+        wall = time.perf_counter() - t
+        runs.append((cb.last_build_timing(), wall))
+    (c, f, tot), wall = min(runs, key=lambda r: r[0][0] + r[0][1])
+    return {"config": "c1: classic, 1,000 docs x 100,000 bp, k=1, p=0.3",
+            "docs_per_s_kernels": cfg.n_docs / ((c + f) / 1e3),
+            "docs_per_s_e2e": cfg.n_docs / (tot / 1e3),
+            "ms_count": c, "ms_fill": f, "ms_total_device_call": tot, "ms_wall": 1e3 * wall}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -69,6 +69,11 @@ int cobs_gpu_index_open(const char* path, int device, cobs_gpu_index** out, char
 int cobs_gpu_index_open_image(const uint8_t* image, uint64_t len, const char* path, int device,
                               cobs_gpu_index** out, char* err, size_t errlen);
 
+/* Launch this handle's work on a caller-owned CUDA stream (a cudaStream_t
+ * passed as void*; NULL restores the handle's own stream), so callers can
+ * bracket batches with their own events.  The caller keeps the stream alive. */
+int cobs_gpu_index_set_stream(cobs_gpu_index* index, void* stream);
+
 /* Releases HBM and host state.  NULL is a no-op. */
 void cobs_gpu_index_close(cobs_gpu_index* index);
 

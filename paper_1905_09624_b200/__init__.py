@@ -143,6 +143,10 @@ class DeviceIndexView:
     def __exit__(self, *exc):
         self.close()
 
+    def set_stream(self, stream_ptr: int) -> None:
+        """Run this index's batches on a caller-owned cudaStream_t."""
+        N.lib.cobs_gpu_index_set_stream(self._h, C.c_void_p(stream_ptr or None))
+
     # IndexView accessors
     def params(self) -> IndexParams:
         c = N.IndexParamsC()

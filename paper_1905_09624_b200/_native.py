@@ -46,6 +46,7 @@ SIGNATURES = {
     "cobs_gpu_index_open_image": (C.c_int, [vp, C.c_uint64, C.c_char_p, C.c_int, C.POINTER(vp),
                                             C.c_char_p, C.c_size_t]),
     "cobs_gpu_index_close": (None, [vp]),
+    "cobs_gpu_index_set_stream": (C.c_int, [vp, vp]),
     "cobs_gpu_index_params": (C.c_int, [vp, C.POINTER(IndexParamsC)]),
     "cobs_gpu_index_kind": (C.c_uint8, [vp]),
     "cobs_gpu_index_block_count": (C.c_uint64, [vp]),

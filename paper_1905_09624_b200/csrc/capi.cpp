@@ -85,6 +85,12 @@ int cobs_gpu_index_open_image(const uint8_t* image, uint64_t len, const char* pa
 
 void cobs_gpu_index_close(cobs_gpu_index* index) { delete index; }
 
+int cobs_gpu_index_set_stream(cobs_gpu_index* index, void* stream) {
+    std::lock_guard<std::mutex> lock(index->ix->mu);
+    index->ix->user_stream = static_cast<cudaStream_t>(stream);
+    return COBS_OK;
+}
+
 int cobs_gpu_index_params(const cobs_gpu_index* index, cobs_index_params* out) {
     const cobsg::Params& P = index->ix->meta.params;
     std::memset(out, 0, sizeof *out);

@@ -43,7 +43,9 @@ struct QueryWorkspace {
 struct DeviceIndex {
     IndexMeta meta;
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // the handle's own stream
+    cudaStream_t user_stream = nullptr; // caller-owned override
+    cudaStream_t work_stream() const { return user_stream ? user_stream : stream; }
     uint8_t* payload = nullptr; // pitched rows of every block
     uint64_t payload_bytes = 0;
     std::vector<DevBlock> blocks;

@@ -383,7 +383,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     std::lock_guard<std::mutex> lock(ix.mu);
     COBS_CUDA(cudaSetDevice(ix.device));
     QueryWorkspace& ws = ix.ws;
-    cudaStream_t st = ix.stream;
+    cudaStream_t st = ix.work_stream();
     const Params& P = ix.meta.params;
     const uint32_t q = P.q, k = P.k;
     const uint64_t D = ix.meta.total_docs();
@@ -394,8 +394,11 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
 
     // Host-side window accounting (needs the offsets on the host).
     std::vector<uint64_t> h_off(n + 1);
-    if (dev_in)
-        COBS_CUDA(cudaMemcpy(h_off.data(), offsets, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    if (dev_in) {
+        COBS_CUDA(cudaMemcpyAsync(h_off.data(), offsets, sizeof(uint64_t) * (n + 1),
+                                  cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+    }
     else
         std::copy(offsets, offsets + n + 1, h_off.begin());
     std::vector<uint64_t> win_base(n + 1), tab_off(n);
