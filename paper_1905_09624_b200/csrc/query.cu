@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "../../include/cobs_gpu.h"
 #include "index.hpp"
@@ -165,6 +166,13 @@ __device__ __forceinline__ uint32_t ld_row(const uint8_t* p, uint64_t policy) {
     return v;
 }
 
+// rowbase + row * pitch in one IMAD.WIDE.U32.
+__device__ __forceinline__ const uint8_t* row_addr(const uint8_t* base, uint32_t row, uint32_t pitch) {
+    const uint8_t* p;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(row), "r"(pitch), "l"(base));
+    return p;
+}
+
 // Bit-sliced counters: a document's count is sum_p 2^p * bit(F[p]).
 template <int NT>
 __device__ __forceinline__ void add_at(uint32_t (&F)[NT], int level, uint32_t x) {
@@ -186,99 +194,153 @@ __device__ __forceinline__ uint32_t extract(const uint32_t (&F)[NT], int i) {
     return s;
 }
 
-// NP: bit planes above the four carry-save levels (NT = NP+4 total; the
-// batch's max window count must be < 2^NT).  KT: k if 1, else 0 (runtime k).
-// EF: L2 evict-first row loads (index far larger than L2).
+// Harley-Seal step: 16 document masks into the carry-save accumulators;
+// returns the weight-16 carry.
+__device__ __forceinline__ uint32_t csa16(const uint32_t* v, uint32_t& ones, uint32_t& twos,
+                                          uint32_t& fours, uint32_t& eights) {
+    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+    csa(twosA, ones, ones, v[0], v[1]);
+    csa(twosB, ones, ones, v[2], v[3]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, v[4], v[5]);
+    csa(twosB, ones, ones, v[6], v[7]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsA, fours, fours, foursA, foursB);
+    csa(twosA, ones, ones, v[8], v[9]);
+    csa(twosB, ones, ones, v[10], v[11]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, v[12], v[13]);
+    csa(twosB, ones, ones, v[14], v[15]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsB, fours, fours, foursA, foursB);
+    csa(sixteens, eights, eights, eightsA, eightsB);
+    return sixteens;
+}
+
+// One warp = one (query, column task): 32 lanes x 4 bytes = the 128-byte,
+// 1024-document slice of every addressed row.  Per chunk of CH terms the
+// lanes compute the CH rows (exact modulo, one term per lane) into a
+// warp-private shared-memory list, then every lane issues CH independent
+// 4-byte loads (each warp load = one coalesced 128-byte line), reading the
+// row list with 128-bit broadcast LDS; the next chunk's hashes are
+// prefetched while this chunk's rows are in flight.
+//
+// NT = NP + 4 bit planes in total (the batch's max window count is < 2^NT).
+// KT = 1: k = 1 and every width < 2^32 (32-bit rows); KT = 0: runtime k,
+// 64-bit rows.  EF: L2 evict-first row loads (index far larger than L2).
 template <int NP, int KT, bool EF>
 __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
     constexpr int NT = NP + 4;
+    constexpr int CH = NT <= 16 ? 32 : 16;    // terms per chunk
+    constexpr int LCH = CH == 32 ? 5 : 4;     // log2(CH): weight of the planes P
+    constexpr int NPP = NT - LCH;             // planes above the carry-save levels
+    using RowT = typename std::conditional<KT == 1, uint32_t, uint64_t>::type;
+    __shared__ __align__(16) RowT s_rows[8][CH];
+
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t groups = (a.qt + 7) / 8;
-    const uint64_t per_tile = groups * a.nct;
-    const uint64_t bid = blockIdx.x;
-    const uint64_t tile = bid / per_tile;
-    const uint64_t r = bid - tile * per_tile;
-    const uint32_t cti = static_cast<uint32_t>(r / groups);
-    const uint64_t qg = r - static_cast<uint64_t>(cti) * groups;
-    const uint64_t qin = qg * 8 + warp;
-    const uint64_t qi = tile * a.qt + qin;
+    const uint32_t groups = (a.qt + 7) / 8;
+    const uint32_t per_tile = groups * a.nct;
+    const uint32_t bid = blockIdx.x;
+    const uint32_t tile = bid / per_tile;
+    const uint32_t r = bid - tile * per_tile;
+    const uint32_t cti = r / groups;
+    const uint32_t qg = r - cti * groups;
+    const uint32_t qin = qg * 8 + warp;
+    const uint64_t qi = static_cast<uint64_t>(tile) * a.qt + qin;
     if (qin >= a.qt || qi >= a.n) return;
     const uint32_t ell = a.ell[qi];
     if (ell == 0) return; // DataError query: no scores, no hits
     const uint32_t k = KT ? KT : a.k;
     const DevBlock B = a.blocks[a.ct[2 * cti]];
     const uint32_t slice = a.ct[2 * cti + 1];
-    const uint32_t lane_byte = slice * 128u + lane * 4u;
-    const bool lane_ok = lane_byte < B.pitch;
+    // Lanes past the row's pitch re-read an in-row word: their documents are
+    // >= doc_count and are masked out below, so no per-load predicate.
+    const uint32_t lane_byte = min(slice * 128u + lane * 4u, B.pitch - 4u);
     const uint8_t* rowbase = a.payload + B.base + lane_byte;
     const uint64_t* hq = a.hashes + a.win_base[qi] * k;
     uint64_t policy = 0;
     if (EF) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    RowT* rows = s_rows[warp];
 
-    uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
-    uint32_t P[NP];
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, sixteens = 0;
+    uint32_t P[NPP];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) P[p] = 0;
+    for (int p = 0; p < NPP; ++p) P[p] = 0;
 
-    const uint32_t hl = lane & 15u;
-    for (uint32_t t0 = 0; t0 < ell; t0 += 16) {
-        const uint32_t tl = t0 + hl;
-        const bool tv = tl < ell;
-        uint32_t v[16];
-        {
-            uint64_t off = tv ? fastmod(__ldg(hq + (uint64_t)tl * k), B.w, B.magic) * B.pitch : 0;
+    uint64_t hnext = 0;
+    if (KT == 1 && lane < CH && lane < ell) hnext = __ldg(hq + lane);
+    // One chunk of CH terms; TAIL (the last, partial chunk only) zeroes the
+    // masks of the padding terms, so full chunks carry no per-term predicate.
+    auto chunk = [&](uint32_t t0, auto tail_c) {
+        constexpr bool TAIL = decltype(tail_c)::value;
+        const uint32_t tl = t0 + lane;
+        uint32_t v[CH];
+        if (KT == 1) {
+            const uint64_t h = hnext;
+            if (lane < CH && tl + CH < ell) hnext = __ldg(hq + tl + CH); // prefetch next chunk
+            if (lane < CH) rows[lane] = (!TAIL || tl < ell) ? static_cast<RowT>(fastmod(h, B.w, B.magic)) : 0;
+            __syncwarp();
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                uint64_t o = __shfl_sync(0xffffffffu, off, u);
-                v[u] = (lane_ok && t0 + u < ell) ? ld_row<EF>(rowbase + o, policy) : 0u;
+            for (int u = 0; u < CH; u += 4) {
+                const uint4 r4 = *reinterpret_cast<const uint4*>(rows + u);
+                v[u + 0] = ld_row<EF>(row_addr(rowbase, r4.x, B.pitch), policy);
+                v[u + 1] = ld_row<EF>(row_addr(rowbase, r4.y, B.pitch), policy);
+                v[u + 2] = ld_row<EF>(row_addr(rowbase, r4.z, B.pitch), policy);
+                v[u + 3] = ld_row<EF>(row_addr(rowbase, r4.w, B.pitch), policy);
+            }
+            __syncwarp();
+        } else {
+            for (uint32_t s = 0; s < k; ++s) { // AND the k rows: query.cpp:65-73
+                if (lane < CH)
+                    rows[lane] = (!TAIL || tl < ell)
+                                     ? static_cast<RowT>(fastmod(__ldg(hq + (uint64_t)tl * k + s), B.w, B.magic))
+                                     : 0;
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < CH; u += 2) {
+                    const ulonglong2 r2 = *reinterpret_cast<const ulonglong2*>(rows + u);
+                    uint32_t x0 = ld_row<EF>(rowbase + r2.x * B.pitch, policy);
+                    uint32_t x1 = ld_row<EF>(rowbase + r2.y * B.pitch, policy);
+                    v[u] = s ? (v[u] & x0) : x0;
+                    v[u + 1] = s ? (v[u + 1] & x1) : x1;
+                }
+                __syncwarp();
             }
         }
-        for (uint32_t s = 1; s < k; ++s) { // AND the k rows: query.cpp:65-73
-            uint64_t off =
-                tv ? fastmod(__ldg(hq + (uint64_t)tl * k + s), B.w, B.magic) * B.pitch : 0;
+        if constexpr (TAIL) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                uint64_t o = __shfl_sync(0xffffffffu, off, u);
-                v[u] &= (lane_ok && t0 + u < ell) ? ld_row<EF>(rowbase + o, policy) : 0u;
-            }
+            for (int u = 0; u < CH; ++u)
+                if (t0 + u >= ell) v[u] = 0;
         }
-        // Harley-Seal: 16 masks -> ones/twos/fours/eights + one weight-16 mask
-        uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
-        csa(twosA, ones, ones, v[0], v[1]);
-        csa(twosB, ones, ones, v[2], v[3]);
-        csa(foursA, twos, twos, twosA, twosB);
-        csa(twosA, ones, ones, v[4], v[5]);
-        csa(twosB, ones, ones, v[6], v[7]);
-        csa(foursB, twos, twos, twosA, twosB);
-        csa(eightsA, fours, fours, foursA, foursB);
-        csa(twosA, ones, ones, v[8], v[9]);
-        csa(twosB, ones, ones, v[10], v[11]);
-        csa(foursA, twos, twos, twosA, twosB);
-        csa(twosA, ones, ones, v[12], v[13]);
-        csa(twosB, ones, ones, v[14], v[15]);
-        csa(foursB, twos, twos, twosA, twosB);
-        csa(eightsB, fours, fours, foursA, foursB);
-        csa(sixteens, eights, eights, eightsA, eightsB);
+        uint32_t carry = csa16(v, ones, twos, fours, eights);
+        if constexpr (CH == 32) {
+            uint32_t c2 = csa16(v + 16, ones, twos, fours, eights);
+            csa(carry, sixteens, sixteens, carry, c2); // carry now has weight 32
+        }
 #pragma unroll
-        for (int p = 0; p < NP; ++p) { // ripple the weight-16 mask
-            uint32_t c = P[p] & sixteens;
-            P[p] ^= sixteens;
-            sixteens = c;
+        for (int p = 0; p < NPP; ++p) { // ripple the weight-CH carry
+            uint32_t c = P[p] & carry;
+            P[p] ^= carry;
+            carry = c;
         }
-    }
+    };
+    uint32_t t0 = 0;
+    for (; t0 + CH <= ell; t0 += CH) chunk(t0, std::false_type{});
+    if (t0 < ell) chunk(t0, std::true_type{});
     // Flush the carry-save state into plain bit planes F (weight 2^p).
     uint32_t F[NT];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) F[p] = 0;
+    for (int p = 0; p < LCH; ++p) F[p] = 0;
 #pragma unroll
-    for (int p = 0; p < NP; ++p) F[p + 4] = P[p];
+    for (int p = 0; p < NPP; ++p) F[p + LCH] = P[p];
+    if constexpr (CH == 32) add_at<NT>(F, 4, sixteens);
     add_at<NT>(F, 3, eights);
     add_at<NT>(F, 2, fours);
     add_at<NT>(F, 1, twos);
     add_at<NT>(F, 0, ones);
 
     // Documents d < dc only: padding columns never count (query.cpp:84-86).
-    const uint32_t d0 = slice * 1024u + lane * 32u;
+    const uint32_t d0 = slice * 1024u + lane * 32u; // this lane's first document
     uint32_t valid = 0;
     if (d0 < B.dc) valid = (B.dc - d0 >= 32u) ? 0xffffffffu : ((1u << (B.dc - d0)) - 1u);
     const uint64_t gdoc0 = static_cast<uint64_t>(B.doc_base) + d0;
@@ -363,16 +425,16 @@ int bits_for(uint64_t v) { // bits to represent values 0..v
 using GatherFn = void (*)(GatherArgs);
 
 template <int NP>
-GatherFn pick_k(uint32_t k, bool ef) {
-    if (k == 1) return ef ? gather_kernel<NP, 1, true> : gather_kernel<NP, 1, false>;
+GatherFn pick_k(bool k1_w32, bool ef) {
+    if (k1_w32) return ef ? gather_kernel<NP, 1, true> : gather_kernel<NP, 1, false>;
     return ef ? gather_kernel<NP, 0, true> : gather_kernel<NP, 0, false>;
 }
 
-GatherFn pick_gather(int nt_needed, uint32_t k, bool ef) {
-    if (nt_needed <= 8) return pick_k<4>(k, ef);
-    if (nt_needed <= 12) return pick_k<8>(k, ef);
-    if (nt_needed <= 16) return pick_k<12>(k, ef);
-    return pick_k<28>(k, ef);
+GatherFn pick_gather(int nt_needed, bool k1_w32, bool ef) {
+    if (nt_needed <= 8) return pick_k<4>(k1_w32, ef);
+    if (nt_needed <= 12) return pick_k<8>(k1_w32, ef);
+    if (nt_needed <= 16) return pick_k<12>(k1_w32, ef);
+    return pick_k<28>(k1_w32, ef);
 }
 
 } // namespace
@@ -512,7 +574,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ga.tau = ws.tau.as<uint32_t>();
     ga.n = n;
     ga.k = k;
-    uint64_t qt = 2048;
+    uint64_t qt = 8192;
     if (const char* e = std::getenv("COBS_QT")) qt = std::max<uint64_t>(8, std::strtoull(e, nullptr, 10));
     qt = std::min<uint64_t>((qt + 7) / 8 * 8, (n + 7) / 8 * 8);
     ga.qt = static_cast<uint32_t>(qt);
@@ -521,7 +583,9 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ga.want_hits = want_hits ? 1 : 0;
     ga.hit_count = ws.hit_count.as<uint32_t>();
     ga.hit_total = ws.hit_total.as<unsigned long long>();
-    GatherFn fn = pick_gather(nt_needed, k, ix.evict_first);
+    bool w32 = true;
+    for (const DevBlock& d : ix.blocks) w32 &= d.w <= 0xffffffffull;
+    GatherFn fn = pick_gather(nt_needed, k == 1 && w32, ix.evict_first);
     const uint64_t tiles = (n + qt - 1) / qt;
     const uint64_t grid2 = tiles * ((qt + 7) / 8) * ga.nct;
     if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
