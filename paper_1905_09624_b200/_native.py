@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcobs_gpu.so")
+LIB_PATH = os.environ.get("COBS_GPU_LIB") or os.path.join(_HERE, "_lib", "libcobs_gpu.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

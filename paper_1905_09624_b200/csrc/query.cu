@@ -25,6 +25,9 @@ namespace cobsg {
 
 namespace {
 
+#ifndef COBS_GATHER_MINB
+#define COBS_GATHER_MINB 3
+#endif
 constexpr int kTermizeThreads = 256;
 constexpr uint32_t kSmemSlots = 8192; // 64 KB of shared set per CTA
 constexpr uint64_t kNoGtab = ~0ull;
@@ -229,7 +232,7 @@ __device__ __forceinline__ uint32_t csa16(const uint32_t* v, uint32_t& ones, uin
 // KT = 1: k = 1 and every width < 2^32 (32-bit rows); KT = 0: runtime k,
 // 64-bit rows.  EF: L2 evict-first row loads (index far larger than L2).
 template <int NP, int KT, bool EF>
-__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+__global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArgs a) {
     constexpr int NT = NP + 4;
     constexpr int CH = NT <= 16 ? 32 : 16;    // terms per chunk
     constexpr int LCH = CH == 32 ? 5 : 4;     // log2(CH): weight of the planes P
