@@ -154,10 +154,6 @@ def workload_name(cfg):
             f"{cfg.n_queries} x {cfg.qlen}-bp queries, K={cfg.K}")
 
 
-def rank_query_ids(cfg, rank):
-    return np.arange(rank * cfg.n_queries, (rank + 1) * cfg.n_queries, dtype=np.uint64)
-
-
 def build_c1_index(cfg, device):
     """Config-1 index built on the device from the seeded corpus."""
     import paper_1905_09624_b200 as cb
@@ -186,7 +182,7 @@ def run_reference(args):
         ref = O.RefIndex.c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma,
                             cfg.p, materialise=True, threads=cores)
         setup_s = time.perf_counter() - t0
-        per_step = args.cpu_sample or 2 * cores
+        per_step = args.cpu_sample or 16 * cores
         K = cfg.K
     else:
         cfg = synth.CONFIGS["c1"]
@@ -276,7 +272,8 @@ def run_gpu(args):
     stream = torch.cuda.Stream(device=local)
     view.set_stream(stream.cuda_stream)
 
-    ids = rank_query_ids(cfg, rank) if cfg.name == "c5" else np.arange(cfg.n_queries, dtype=np.uint64)
+    from paper_1905_09624_b200.dist import reduce_max, reduce_sum, weak_query_ids
+    ids = weak_query_ids(cfg.n_queries, rank) if cfg.name == "c5" else np.arange(cfg.n_queries, dtype=np.uint64)
     qb, qo = synth.queries(cfg, ids)
     n = len(qo) - 1
     h_pat = torch.from_numpy(qb).pin_memory()
@@ -307,11 +304,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        ms = e0.elapsed_time(e1) / steps
-        if dist:
-            t = torch.tensor([ms], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = reduce_max(e0.elapsed_time(e1) / steps, f"cuda:{local}")  # max over ranks
         return ms, outs
 
     clocks = ClockSampler(local)
@@ -321,11 +314,7 @@ def run_gpu(args):
     clk = clocks.stop()
 
     grams = int(outs[-1].ell.astype(np.uint64).sum())
-    total_grams = grams
-    if dist:
-        t = torch.tensor([grams], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t)
-        total_grams = int(t.item())
+    total_grams = int(reduce_sum(grams, f"cuda:{local}"))  # q-grams of all ranks
     value = total_grams / (ms_dev / 1e3)
     e2e_value = total_grams / (ms_e2e / 1e3)
     last = outs_e2e[-1]

@@ -1,0 +1,83 @@
+"""Multi-rank host logic on CPU with the gloo backend, world_size 2."""
+import os
+import random
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1905_09624_b200.dist import shard_range, weak_query_ids
+
+
+def test_shard_range_partitions():
+    for n in (0, 1, 7, 100, 101):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_weak_ids_disjoint():
+    a, b = weak_query_ids(5, 0), weak_query_ids(5, 1)
+    assert set(a).isdisjoint(b) and len(a) == len(b) == 5
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, img, pats, q):
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_1905_09624_b200.dist import gather_results, reduce_max, shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # this rank's contiguous share of the batch; the CPU oracle stands in for
+    # the per-rank engine (no GPU here) -- the merge logic is what is tested
+    lo, hi = shard_range(len(pats), rank, world)
+    idx = O.OracleIndex.parse(img)
+    ell, hn, docs, scores = [], [], [], []
+    for p in pats[lo:hi]:
+        e, s, h, _ = idx.query(p, 0.5)
+        ell.append(e)
+        hn.append(len(h))
+        docs += [d for d, _ in h]
+        scores += [sc for _, sc in h]
+    merged = gather_results(np.asarray(ell, np.uint64), np.asarray(hn, np.uint64),
+                            np.asarray(docs, np.int64), np.asarray(scores, np.uint64))
+    t = reduce_max(float(rank + 1))
+    if rank == 0:
+        q.put((merged, t))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_equals_single_rank():
+    from oracle import oracle as O
+    rng = random.Random(3)
+    docs = [(b"doc%04d" % i, [bytes(rng.choice(b"ACGT") for _ in range(rng.randint(100, 900)))])
+            for i in range(15)]
+    img = O.build_image(docs, k=2, block_size=4, kind=1)
+    pats = [docs[i % 15][1][0][: 80 + i] for i in range(9)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_worker, args=(2, _free_port(), img, pats, q), nprocs=2, join=True,
+                       start_method="spawn")
+    merged, tmax = q.get(timeout=60)
+    assert tmax == 2.0
+    idx = O.OracleIndex.parse(img)
+    want_docs, want_n = [], []
+    for p in pats:
+        e, s, h, _ = idx.query(p, 0.5)
+        want_n.append(len(h))
+        want_docs += [d for d, _ in h]
+    assert list(merged["hit_n"]) == want_n
+    assert list(merged["docs"]) == want_docs
