@@ -101,6 +101,11 @@ int cobs_gpu_index_row(const cobs_gpu_index* index, uint64_t block, uint64_t r, 
  * read back from HBM and the file is byte-identical to the reference's. */
 int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* err, size_t errlen);
 
+/* The same bytes as cobs_gpu_index_write, returned in memory (free with
+ * cobs_gpu_free). */
+int cobs_gpu_index_image(const cobs_gpu_index* index, uint8_t** image, uint64_t* image_len, char* err,
+                         size_t errlen);
+
 /* ---- batch query ------------------------------------------------------ */
 
 /* flags */
@@ -169,6 +174,18 @@ int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_
                    const cobs_index_params* params, int kind, uint64_t forced_w, int device,
                    const char* out_path, uint8_t** image, uint64_t* image_len, char* err,
                    size_t errlen);
+
+/* build flags */
+#define COBS_B_DEVICE_INPUT 1u /* `seqs` is a device pointer (seg/doc arrays stay on the host) */
+
+/* cobs_gpu_build with flags, optionally returning the built index resident
+ * in HBM (`index_out`, ready to query; close with cobs_gpu_index_close)
+ * instead of, or as well as, the file image / file. */
+int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_segs,
+                      const uint64_t* doc_segs, const char* const* names, uint64_t n_docs,
+                      const cobs_index_params* params, int kind, uint64_t forced_w, int device,
+                      uint32_t flags, const char* out_path, uint8_t** image, uint64_t* image_len,
+                      cobs_gpu_index** index_out, char* err, size_t errlen);
 
 /* Build timings (ms) of the calling thread's last cobs_gpu_build: term
  * counting, fill (sequences in HBM -> finished matrix), total incl. H2D,

@@ -241,6 +241,20 @@ def write_index(view: DeviceIndexView, path: str) -> None:
         _raise(rc, err)
 
 
+def index_image(view: DeviceIndexView) -> bytes:
+    """The file image of a device-resident index (write_index into memory)."""
+    img = C.c_void_p()
+    ln = C.c_uint64()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_index_image(view._h, C.byref(img), C.byref(ln), err, len(err))
+    if rc:
+        _raise(rc, err)
+    try:
+        return C.string_at(img, ln.value)
+    finally:
+        N.lib.cobs_gpu_free(img)
+
+
 def pack_patterns(patterns: Sequence[bytes]) -> Tuple[np.ndarray, np.ndarray]:
     """Concatenate patterns into (bytes, offsets[n+1])."""
     lens = np.fromiter((len(p) for p in patterns), dtype=np.uint64, count=len(patterns))
@@ -389,6 +403,48 @@ def build_compact(docs: Sequence[Document], params: IndexParams = IndexParams(),
                   path: Optional[str] = None, device: int = 0) -> bytes:
     """build_compact (compact_index.hpp:26-27) + write_index."""
     return build_image(docs, params, KIND_COMPACT, 0, path, device)
+
+
+def build_device(seqs, seg_off: np.ndarray, doc_segs: np.ndarray, names: Sequence[bytes],
+                 params: IndexParams, kind: int, forced_w: int = 0, device: int = 0,
+                 seqs_on_device: bool = False, want_image: bool = False,
+                 path: Optional[str] = None) -> Tuple[DeviceIndexView, Optional[bytes]]:
+    """Build and keep the index resident in HBM (ready to query).  ``seqs`` is
+    a host numpy uint8 array or, with seqs_on_device, a device address."""
+    seg_off = np.ascontiguousarray(seg_off, np.uint64)
+    doc_segs = np.ascontiguousarray(doc_segs, np.uint64)
+    nm = (C.c_char_p * max(len(names), 1))(*[n if isinstance(n, bytes) else n.encode() for n in names])
+    h = C.c_void_p()
+    img = C.c_void_p()
+    ln = C.c_uint64()
+    err = _errbuf()
+    cp = params._c()
+    sp = seqs if seqs_on_device else np.ascontiguousarray(seqs, np.uint8).ctypes.data
+    rc = N.lib.cobs_gpu_build_ex(sp, seg_off.ctypes.data, len(seg_off) - 1, doc_segs.ctypes.data,
+                                 nm, len(names), C.byref(cp), kind, forced_w, device,
+                                 N.B_DEVICE_INPUT if seqs_on_device else 0,
+                                 str(path).encode() if path else None,
+                                 C.byref(img) if want_image else None,
+                                 C.byref(ln) if want_image else None, C.byref(h), err, len(err))
+    if rc:
+        _raise(rc, err)
+    image = None
+    if want_image:
+        try:
+            image = C.string_at(img, ln.value)
+        finally:
+            N.lib.cobs_gpu_free(img)
+    return DeviceIndexView(h.value), image
+
+
+def synth_docs_device(seed: int, alpha: int, lengths: np.ndarray, dev_ptr: int, device: int = 0,
+                      lo: int = 0, hi: Optional[int] = None) -> None:
+    """Generate seeded documents [lo, hi) straight into device memory."""
+    lengths = np.ascontiguousarray(lengths, np.uint64)
+    hi = len(lengths) if hi is None else hi
+    rc = N.lib.cobs_gpu_synth_docs(seed, alpha, lengths.ctypes.data, lo, hi, dev_ptr, device)
+    if rc:
+        raise CudaError("synth_docs failed")
 
 
 def last_build_timing() -> Tuple[float, float, float]:

@@ -60,6 +60,8 @@ SIGNATURES = {
     "cobs_gpu_index_device_bytes": (C.c_uint64, [vp]),
     "cobs_gpu_index_row": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
     "cobs_gpu_index_write": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_size_t]),
+    "cobs_gpu_index_image": (C.c_int, [vp, C.POINTER(vp), C.POINTER(C.c_uint64), C.c_char_p,
+                                       C.c_size_t]),
     "cobs_gpu_query_batch": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_double, C.c_uint64, C.c_uint32,
                                        C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_results_count": (C.c_uint64, [vp]),
@@ -80,6 +82,10 @@ SIGNATURES = {
     "cobs_gpu_build": (C.c_int, [vp, vp, C.c_uint64, vp, C.POINTER(C.c_char_p), C.c_uint64,
                                  C.POINTER(IndexParamsC), C.c_int, C.c_uint64, C.c_int, C.c_char_p,
                                  C.POINTER(vp), C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
+    "cobs_gpu_build_ex": (C.c_int, [vp, vp, C.c_uint64, vp, C.POINTER(C.c_char_p), C.c_uint64,
+                                    C.POINTER(IndexParamsC), C.c_int, C.c_uint64, C.c_int,
+                                    C.c_uint32, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_uint64),
+                                    C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_build_timing": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]),
     "cobs_gpu_free": (None, [vp]),
@@ -95,3 +101,4 @@ for _name, (_res, _args) in SIGNATURES.items():
 
 OK, EUSAGE, EDATA, ECUDA = 0, 1, 2, 4
 Q_HITS, Q_SCORES, Q_DEVICE_INPUT, Q_KEEP_DEVICE = 1, 2, 4, 8
+B_DEVICE_INPUT = 1

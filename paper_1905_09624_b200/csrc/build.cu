@@ -10,8 +10,9 @@
 //               compact_index.cpp:19-52, bloom.cpp:50-66)
 //   fill pass   one thread per window and seed: atomicOr of bit
 //               (XXH64 % w_b, column) into the block's row-major matrix,
-//               stored unpitched at exactly the file's payload layout so the
-//               D2H copy IS the payload   (classic_index.cpp:26-36,
+//               written straight into the pitched HBM layout of the query
+//               index (so a built index is queryable in place); the file
+//               payload is its un-pitched D2H copy  (classic_index.cpp:26-36,
 //               bit_matrix.hpp:25-27).  OR is idempotent, so every window is
 //               filled, not just the distinct ones.
 #include <algorithm>
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
 }
 
 struct FillBlock {
-    uint64_t base; // payload byte offset of row 0 (file layout)
-    uint64_t w, magic, rb;
+    uint64_t base; // byte offset of row 0 in the pitched payload
+    uint64_t w, magic, rb; // rb: row stride (the device pitch)
 };
 
 __global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* blocks,
@@ -135,9 +136,11 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 
 const BuildTiming& last_build_timing() { return g_timing; }
 
-std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, uint64_t n_segs,
-                                 const uint64_t* doc_segs, const std::vector<std::string>& names,
-                                 const Params& P, uint8_t kind, uint64_t forced_w, int device) {
+std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint64_t* seg_off,
+                                                uint64_t n_segs, const uint64_t* doc_segs,
+                                                const std::vector<std::string>& names, const Params& P,
+                                                uint8_t kind, uint64_t forced_w, int device,
+                                                bool seqs_on_device) {
     auto t_start = std::chrono::steady_clock::now();
     g_timing = BuildTiming();
     P.validate();                                             // params.hpp:26-35
@@ -187,14 +190,15 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
     const uint64_t total_w = seg_wbase[n_segs];
 
     DevBuf d_seqs, d_segoff, d_segw, d_segdoc, d_docstart, d_tab, d_taboff, d_tabslots, d_tc;
-    d_seqs.reserve(std::max<uint64_t>(total_bytes, 1));
+    if (!seqs_on_device) d_seqs.reserve(std::max<uint64_t>(total_bytes, 1));
     d_segoff.reserve(8 * (n_segs + 1));
     d_segw.reserve(8 * (n_segs + 1));
     d_segdoc.reserve(4 * std::max<uint64_t>(n_segs, 1));
     d_docstart.reserve(8 * n_docs);
     d_tc.reserve(8 * n_docs);
     auto t_h2d = std::chrono::steady_clock::now();
-    COBS_CUDA(cudaMemcpyAsync(d_seqs.ptr, seqs, total_bytes, cudaMemcpyHostToDevice, st));
+    if (!seqs_on_device)
+        COBS_CUDA(cudaMemcpyAsync(d_seqs.ptr, seqs, total_bytes, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_segoff.ptr, seg_off, 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_wbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     if (n_segs)
@@ -205,7 +209,7 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
     g_timing.ms_h2d = ms_since(t_h2d);
 
     WinArgs wa{};
-    wa.seqs = d_seqs.as<uint8_t>();
+    wa.seqs = seqs_on_device ? seqs : d_seqs.as<uint8_t>();
     wa.seg_off = d_segoff.as<uint64_t>();
     wa.seg_wbase = d_segw.as<uint64_t>();
     wa.seg_doc = d_segdoc.as<uint32_t>();
@@ -296,39 +300,38 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
         meta.blocks.push_back(bm);
     }
     meta.layout();
-    std::vector<uint8_t> header = meta.header_bytes(); // throws on > 65535-byte names
-    const uint64_t payload = meta.file_size - meta.payload_start;
+    (void)meta.header_bytes(); // DataError for names longer than 65,535 bytes (storage.cpp:368)
 
-    // ---- fill pass ------------------------------------------------------
+    // ---- fill pass, straight into the pitched HBM layout of a DeviceIndex
+    auto ix = std::make_unique<DeviceIndex>();
+    ix->meta = std::move(meta);
+    ix->device = device;
+    ix->allocate(); // refuses a matrix that does not fit in free HBM
+    COBS_CUDA(cudaMemsetAsync(ix->payload, 0, ix->payload_bytes, ix->stream));
+    COBS_CUDA(cudaStreamSynchronize(ix->stream));
     std::vector<FillBlock> fb(nb);
     for (uint64_t b = 0; b < nb; ++b) {
-        fb[b].base = meta.blocks[b].offset - meta.payload_start;
-        fb[b].w = meta.blocks[b].w;
-        fb[b].magic = mod_magic(meta.blocks[b].w);
-        fb[b].rb = meta.blocks[b].row_bytes();
+        fb[b].base = ix->blocks[b].base;
+        fb[b].w = ix->blocks[b].w;
+        fb[b].magic = ix->blocks[b].magic;
+        fb[b].rb = ix->blocks[b].pitch; // row stride on the device
     }
-    DevBuf d_fb, d_dblock, d_dcol, d_words;
+    DevBuf d_fb, d_dblock, d_dcol;
     d_fb.reserve(sizeof(FillBlock) * nb);
     d_dblock.reserve(4 * n_docs);
     d_dcol.reserve(4 * n_docs);
-    size_t free2 = 0;
-    COBS_CUDA(cudaMemGetInfo(&free2, &total_b));
-    if ((payload + 3) / 4 * 4 + (64ull << 20) > free2)
-        throw DataError("index matrix (" + std::to_string(payload) +
-                        " bytes) does not fit in free device memory");
-    d_words.reserve(std::max<uint64_t>((payload + 3) / 4 * 4, 4));
     COBS_CUDA(cudaMemcpyAsync(d_fb.ptr, fb.data(), sizeof(FillBlock) * nb, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_dblock.ptr, doc_block.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_dcol.ptr, doc_col.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaEventRecord(e2, st));
-    COBS_CUDA(cudaMemsetAsync(d_words.ptr, 0, (payload + 3) / 4 * 4, st));
     wa.seg_lo = 0;
     wa.seg_hi = n_segs;
     wa.w_lo = 0;
     wa.w_hi = total_w;
     if (total_w > 0) {
         fill_kernel<<<148 * 16, 256, 0, st>>>(wa, d_fb.as<FillBlock>(), d_dblock.as<uint32_t>(),
-                                              d_dcol.as<uint32_t>(), d_words.as<unsigned int>());
+                                              d_dcol.as<uint32_t>(),
+                                              reinterpret_cast<unsigned int*>(ix->payload));
         COBS_CUDA(cudaGetLastError());
     }
     COBS_CUDA(cudaEventRecord(e3, st));
@@ -336,18 +339,40 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
     float ms_fill = 0;
     cudaEventElapsedTime(&ms_fill, e2, e3);
     g_timing.ms_fill = ms_fill;
-
-    std::vector<uint8_t> image(header.size() + payload);
-    std::memcpy(image.data(), header.data(), header.size());
-    auto t_d2h = std::chrono::steady_clock::now();
-    if (payload)
-        COBS_CUDA(cudaMemcpy(image.data() + header.size(), d_words.ptr, payload, cudaMemcpyDeviceToHost));
-    g_timing.ms_d2h = ms_since(t_d2h);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     cudaEventDestroy(e3);
+    ix->finish_upload();
     g_timing.ms_total = ms_since(t_start);
+    return ix;
+}
+
+std::vector<uint8_t> index_image(const DeviceIndex& ix) {
+    std::vector<uint8_t> header = ix.meta.header_bytes();
+    const uint64_t payload = ix.meta.file_size - ix.meta.payload_start;
+    std::vector<uint8_t> image(header.size() + payload);
+    std::memcpy(image.data(), header.data(), header.size());
+    COBS_CUDA(cudaSetDevice(ix.device));
+    uint64_t off = header.size();
+    for (const DevBlock& d : ix.blocks) { // un-pitch on the copy engine
+        if (d.w)
+            COBS_CUDA(cudaMemcpy2D(image.data() + off, d.rb, ix.payload + d.base, d.pitch, d.rb, d.w,
+                                   cudaMemcpyDeviceToHost));
+        off += d.w * d.rb;
+    }
+    return image;
+}
+
+std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, uint64_t n_segs,
+                                 const uint64_t* doc_segs, const std::vector<std::string>& names,
+                                 const Params& P, uint8_t kind, uint64_t forced_w, int device) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto ix = build_device_index(seqs, seg_off, n_segs, doc_segs, names, P, kind, forced_w, device, false);
+    auto t_d2h = std::chrono::steady_clock::now();
+    std::vector<uint8_t> image = index_image(*ix);
+    g_timing.ms_d2h = ms_since(t_d2h);
+    g_timing.ms_total = ms_since(t0);
     return image;
 }
 

@@ -170,6 +170,19 @@ int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* er
     });
 }
 
+int cobs_gpu_index_image(const cobs_gpu_index* index, uint8_t** image, uint64_t* image_len, char* err,
+                         size_t errlen) {
+    *image = nullptr;
+    *image_len = 0;
+    return guarded(err, errlen, [&] {
+        std::vector<uint8_t> img = cobsg::index_image(*index->ix);
+        *image = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
+        if (!*image) throw std::bad_alloc();
+        std::memcpy(*image, img.data(), img.size());
+        *image_len = img.size();
+    });
+}
+
 int cobs_gpu_query_batch(cobs_gpu_index* index, const uint8_t* patterns, const uint64_t* offsets,
                          uint64_t n, double K, uint64_t top_t, uint32_t flags, cobs_gpu_results** out,
                          char* err, size_t errlen) {
@@ -244,27 +257,45 @@ uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r) { return r->r.row
 
 void cobs_gpu_results_free(cobs_gpu_results* r) { delete r; }
 
+int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_segs,
+                      const uint64_t* doc_segs, const char* const* names, uint64_t n_docs,
+                      const cobs_index_params* params, int kind, uint64_t forced_w, int device,
+                      uint32_t flags, const char* out_path, uint8_t** image, uint64_t* image_len,
+                      cobs_gpu_index** index_out, char* err, size_t errlen) {
+    if (image) *image = nullptr;
+    if (image_len) *image_len = 0;
+    if (index_out) *index_out = nullptr;
+    return guarded(err, errlen, [&] {
+        std::vector<std::string> nm(n_docs);
+        for (uint64_t d = 0; d < n_docs; ++d) nm[d] = names[d];
+        auto ix = cobsg::build_device_index(seqs, seg_offsets, n_segs, doc_segs, nm, to_params(params),
+                                            static_cast<uint8_t>(kind), forced_w, device,
+                                            (flags & COBS_B_DEVICE_INPUT) != 0);
+        if (out_path || image) {
+            std::vector<uint8_t> img = cobsg::index_image(*ix);
+            if (out_path) cobsg::write_image(img, out_path);
+            if (image) {
+                *image = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
+                if (!*image) throw std::bad_alloc();
+                std::memcpy(*image, img.data(), img.size());
+                *image_len = img.size();
+            }
+        }
+        if (index_out) {
+            auto h = std::make_unique<cobs_gpu_index>();
+            h->ix = std::move(ix);
+            *index_out = h.release();
+        }
+    });
+}
+
 int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_segs,
                    const uint64_t* doc_segs, const char* const* names, uint64_t n_docs,
                    const cobs_index_params* params, int kind, uint64_t forced_w, int device,
                    const char* out_path, uint8_t** image, uint64_t* image_len, char* err,
                    size_t errlen) {
-    if (image) *image = nullptr;
-    if (image_len) *image_len = 0;
-    return guarded(err, errlen, [&] {
-        std::vector<std::string> nm(n_docs);
-        for (uint64_t d = 0; d < n_docs; ++d) nm[d] = names[d];
-        std::vector<uint8_t> img = cobsg::build_index(seqs, seg_offsets, n_segs, doc_segs, nm,
-                                                      to_params(params), static_cast<uint8_t>(kind),
-                                                      forced_w, device);
-        if (out_path) cobsg::write_image(img, out_path);
-        if (image) {
-            *image = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
-            if (!*image) throw std::bad_alloc();
-            std::memcpy(*image, img.data(), img.size());
-            *image_len = img.size();
-        }
-    });
+    return cobs_gpu_build_ex(seqs, seg_offsets, n_segs, doc_segs, names, n_docs, params, kind,
+                             forced_w, device, 0, out_path, image, image_len, nullptr, err, errlen);
 }
 
 int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total) {

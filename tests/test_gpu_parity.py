@@ -207,3 +207,31 @@ def test_c5_procedural_small(gpu):
         assert np.array_equal(bres.dense[i].astype(np.uint32), dense)
         assert gpu_hits(view, bres, i) == [list(h) for h in hits]
     view.close()
+
+
+def test_build_device_resident(gpu):
+    """cobs_gpu_build_ex: device-resident sequences in, queryable index out;
+    its image equals the host-input build's and the oracle's."""
+    import torch
+    from paper_1905_09624_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c3"], 150, len_scale=0.001, n_queries=20, block_size=32)
+    lengths = synth.doc_lengths(cfg)
+    dev = torch.empty(int(lengths.sum()), dtype=torch.uint8, device="cuda")
+    cb.synth_docs_device(cfg.seed, cfg.alpha, lengths, dev.data_ptr())
+    torch.cuda.synchronize()
+    host, off = synth.docs(cfg, lengths=lengths)
+    assert np.array_equal(dev.cpu().numpy(), host)  # device generator == host generator
+    names = synth.doc_names(cfg)
+    params = cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p, canonical=cfg.canonical,
+                            block_size=cfg.block_size)
+    view, img = cb.build_device(dev.data_ptr(), off, np.arange(cfg.n_docs + 1), names, params,
+                                cfg.kind, seqs_on_device=True, want_image=True)
+    docs = [(names[i], [host[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
+    want = O.build_image(docs, q=cfg.q, k=cfg.k, p=cfg.p, canonical=True, block_size=32, kind=1)
+    assert img == want and cb.index_image(view) == want
+    qb, qo = synth.queries(cfg, lengths=lengths)
+    got = cb.query_batch_raw(view, qb, qo, 1e-12, scores=True)
+    idx = O.OracleIndex.parse(want)
+    ell, sk, st, nh, dense = idx.query_batch(qb, qo, 1e-12, scores=True)
+    assert np.array_equal(got.dense.astype(np.uint32), dense)
+    view.close()
