@@ -58,6 +58,13 @@ _vp = C.c_void_p
 _u64 = C.c_uint64
 
 
+def _take(ptr, n: int) -> bytes:
+    # ctypes.string_at truncates its size to a C int; copy through numpy
+    if n == 0:
+        return b""
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(n,)).tobytes()
+
+
 def _load_oracle():
     ensure_built()
     L = C.CDLL(ORACLE_SO)
@@ -129,7 +136,7 @@ def extract_terms(content: Sequence[bytes], q: int, canonical: bool) -> Tuple[Li
     ell, sk, occ = _u64(), _u64(), _u64()
     orc().orc_extract_terms(ptrs, lens, len(content), q, 1 if canonical else 0, C.byref(terms),
                             C.byref(ell), C.byref(sk), C.byref(occ))
-    raw = C.string_at(terms, ell.value * q) if ell.value else b""
+    raw = _take(terms, ell.value * q)
     orc().orc_free(terms)
     return [raw[i * q:(i + 1) * q] for i in range(ell.value)], sk.value, occ.value
 
@@ -183,7 +190,7 @@ class OracleIndex:
         p = C.c_void_p()
         n = _u64()
         orc().orc_header_image(C.byref(self.x), C.byref(p), C.byref(n))
-        out = C.string_at(p, n.value)
+        out = _take(p, n.value)
         orc().orc_free(p)
         return out
 
@@ -249,7 +256,7 @@ def build_image(docs: Sequence[Tuple[bytes, Sequence[bytes]]], q=31, k=1, p=0.3,
                                C.byref(img), C.byref(n), err, 512)
     if rc:
         raise OracleError(rc, err.value.decode())
-    out = C.string_at(img, n.value)
+    out = _take(img, n.value)
     orc().orc_free(img)
     return out
 
@@ -401,6 +408,6 @@ def ref_extract_terms(content: Sequence[bytes], q: int, canonical: bool):
                                  C.byref(terms), C.byref(ell), C.byref(sk), C.byref(occ))
     if rc:
         raise OracleError(rc, "extract_terms")
-    raw = C.string_at(terms, ell.value * q) if ell.value else b""
+    raw = _take(terms, ell.value * q)
     ref().ref_free(terms)
     return [raw[i * q:(i + 1) * q] for i in range(ell.value)], sk.value, occ.value

@@ -52,6 +52,14 @@ def _errbuf() -> C.Array:
     return C.create_string_buffer(1024)
 
 
+def _take_bytes(ptr: C.c_void_p, n: int) -> bytes:
+    """Copy n bytes from a library buffer (ctypes.string_at truncates sizes
+    to a C int, so go through a numpy view)."""
+    if n == 0:
+        return b""
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(n,)).tobytes()
+
+
 @dataclass
 class IndexParams:
     """proj/include/cobs/params.hpp:17-38."""
@@ -250,7 +258,7 @@ def index_image(view: DeviceIndexView) -> bytes:
     if rc:
         _raise(rc, err)
     try:
-        return C.string_at(img, ln.value)
+        return _take_bytes(img, ln.value)
     finally:
         N.lib.cobs_gpu_free(img)
 
@@ -388,7 +396,7 @@ def build_image(docs: Sequence[Document], params: IndexParams, kind: int, forced
     if rc:
         _raise(rc, err)
     try:
-        return C.string_at(img, ln.value)
+        return _take_bytes(img, ln.value)
     finally:
         N.lib.cobs_gpu_free(img)
 
@@ -431,7 +439,7 @@ def build_device(seqs, seg_off: np.ndarray, doc_segs: np.ndarray, names: Sequenc
     image = None
     if want_image:
         try:
-            image = C.string_at(img, ln.value)
+            image = _take_bytes(img, ln.value)
         finally:
             N.lib.cobs_gpu_free(img)
     return DeviceIndexView(h.value), image
