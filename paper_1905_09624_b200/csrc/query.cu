@@ -234,11 +234,12 @@ __device__ __forceinline__ uint32_t csa16(const uint32_t* v, uint32_t& ones, uin
 template <int NP, int KT, bool EF>
 __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArgs a) {
     constexpr int NT = NP + 4;
-    constexpr int CH = NT <= 16 ? 32 : 16;    // terms per chunk
+    constexpr int CH = (NT <= 16 && KT == 1) ? 32 : 16; // terms per chunk
     constexpr int LCH = CH == 32 ? 5 : 4;     // log2(CH): weight of the planes P
     constexpr int NPP = NT - LCH;             // planes above the carry-save levels
-    using RowT = typename std::conditional<KT == 1, uint32_t, uint64_t>::type;
-    __shared__ __align__(16) RowT s_rows[8][CH];
+    constexpr int KS = KT ? KT : 1;           // row lists per chunk held in smem
+    using RowT = typename std::conditional<KT != 0, uint32_t, uint64_t>::type;
+    __shared__ __align__(16) RowT s_rows[8][KS * CH];
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t groups = (a.qt + 7) / 8;
@@ -270,26 +271,46 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
 #pragma unroll
     for (int p = 0; p < NPP; ++p) P[p] = 0;
 
-    uint64_t hnext = 0;
-    if (KT == 1 && lane < CH && lane < ell) hnext = __ldg(hq + lane);
+    uint64_t hnext[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s)
+        hnext[s] = (KT != 0 && lane < CH && lane < ell) ? __ldg(hq + (uint64_t)lane * KS + s) : 0;
     // One chunk of CH terms; TAIL (the last, partial chunk only) zeroes the
     // masks of the padding terms, so full chunks carry no per-term predicate.
     auto chunk = [&](uint32_t t0, auto tail_c) {
         constexpr bool TAIL = decltype(tail_c)::value;
         const uint32_t tl = t0 + lane;
         uint32_t v[CH];
-        if (KT == 1) {
-            const uint64_t h = hnext;
-            if (lane < CH && tl + CH < ell) hnext = __ldg(hq + tl + CH); // prefetch next chunk
-            if (lane < CH) rows[lane] = (!TAIL || tl < ell) ? static_cast<RowT>(fastmod(h, B.w, B.magic)) : 0;
+        if constexpr (KT != 0) { // k = KT, 32-bit rows; the k rows are ANDed (query.cpp:65-73)
+            uint64_t h[KS];
+#pragma unroll
+            for (int s = 0; s < KS; ++s) h[s] = hnext[s];
+            if (lane < CH && tl + CH < ell) { // prefetch the next chunk's hashes
+#pragma unroll
+                for (int s = 0; s < KS; ++s) hnext[s] = __ldg(hq + (uint64_t)(tl + CH) * KS + s);
+            }
+            if (lane < CH) {
+#pragma unroll
+                for (int s = 0; s < KS; ++s)
+                    rows[s * CH + lane] =
+                        (!TAIL || tl < ell) ? static_cast<RowT>(fastmod(h[s], B.w, B.magic)) : 0;
+            }
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < CH; u += 4) {
-                const uint4 r4 = *reinterpret_cast<const uint4*>(rows + u);
+                uint4 r4 = *reinterpret_cast<const uint4*>(rows + u);
                 v[u + 0] = ld_row<EF>(row_addr(rowbase, r4.x, B.pitch), policy);
                 v[u + 1] = ld_row<EF>(row_addr(rowbase, r4.y, B.pitch), policy);
                 v[u + 2] = ld_row<EF>(row_addr(rowbase, r4.z, B.pitch), policy);
                 v[u + 3] = ld_row<EF>(row_addr(rowbase, r4.w, B.pitch), policy);
+#pragma unroll
+                for (int s = 1; s < KS; ++s) {
+                    r4 = *reinterpret_cast<const uint4*>(rows + s * CH + u);
+                    v[u + 0] &= ld_row<EF>(row_addr(rowbase, r4.x, B.pitch), policy);
+                    v[u + 1] &= ld_row<EF>(row_addr(rowbase, r4.y, B.pitch), policy);
+                    v[u + 2] &= ld_row<EF>(row_addr(rowbase, r4.z, B.pitch), policy);
+                    v[u + 3] &= ld_row<EF>(row_addr(rowbase, r4.w, B.pitch), policy);
+                }
             }
             __syncwarp();
         } else {
@@ -427,17 +448,27 @@ int bits_for(uint64_t v) { // bits to represent values 0..v
 
 using GatherFn = void (*)(GatherArgs);
 
-template <int NP>
-GatherFn pick_k(bool k1_w32, bool ef) {
-    if (k1_w32) return ef ? gather_kernel<NP, 1, true> : gather_kernel<NP, 1, false>;
-    return ef ? gather_kernel<NP, 0, true> : gather_kernel<NP, 0, false>;
+template <int NP, int KT>
+GatherFn pick_ef(bool ef) {
+    return ef ? gather_kernel<NP, KT, true> : gather_kernel<NP, KT, false>;
 }
 
-GatherFn pick_gather(int nt_needed, bool k1_w32, bool ef) {
-    if (nt_needed <= 8) return pick_k<4>(k1_w32, ef);
-    if (nt_needed <= 12) return pick_k<8>(k1_w32, ef);
-    if (nt_needed <= 16) return pick_k<12>(k1_w32, ef);
-    return pick_k<28>(k1_w32, ef);
+// kt: 1..3 with every width < 2^32 (32-bit rows), else 0 (runtime k, 64-bit rows)
+template <int NP>
+GatherFn pick_k(int kt, bool ef) {
+    switch (kt) {
+    case 1: return pick_ef<NP, 1>(ef);
+    case 2: return pick_ef<NP, 2>(ef);
+    case 3: return pick_ef<NP, 3>(ef);
+    default: return pick_ef<NP, 0>(ef);
+    }
+}
+
+GatherFn pick_gather(int nt_needed, int kt, bool ef) {
+    if (nt_needed <= 8) return pick_k<4>(kt, ef);
+    if (nt_needed <= 12) return pick_k<8>(kt, ef);
+    if (nt_needed <= 16) return pick_k<12>(kt, ef);
+    return pick_k<28>(kt, ef);
 }
 
 } // namespace
@@ -588,7 +619,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ga.hit_total = ws.hit_total.as<unsigned long long>();
     bool w32 = true;
     for (const DevBlock& d : ix.blocks) w32 &= d.w <= 0xffffffffull;
-    GatherFn fn = pick_gather(nt_needed, k == 1 && w32, ix.evict_first);
+    GatherFn fn = pick_gather(nt_needed, (w32 && k <= 3) ? static_cast<int>(k) : 0, ix.evict_first);
     const uint64_t tiles = (n + qt - 1) / qt;
     const uint64_t grid2 = tiles * ((qt + 7) / 8) * ga.nct;
     if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
