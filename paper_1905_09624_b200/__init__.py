@@ -310,14 +310,11 @@ def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: 
         res_ell = arr(ell, n, np.uint32)
         res_sk = arr(sk, n, np.uint64)
         res_st = arr(st, n, np.int32)
-        messages = []
-        for i in range(n):
-            if res_st[i]:
-                msg = C.c_char_p()
-                N.lib.cobs_gpu_results_query(r, i, None, None, None, C.byref(msg), None)
-                messages.append(msg.value.decode())
-            else:
-                messages.append("")
+        messages = [""] * n
+        for i in np.nonzero(res_st)[0].tolist():  # only the failed queries carry text
+            msg = C.c_char_p()
+            N.lib.cobs_gpu_results_query(r, i, None, None, None, C.byref(msg), None)
+            messages[i] = msg.value.decode()
         dense = None
         if scores and not keep_device:
             sb = C.c_uint32()
