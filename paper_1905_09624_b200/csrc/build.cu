@@ -32,24 +32,26 @@ namespace {
 
 thread_local BuildTiming g_timing;
 
+constexpr int kBRun = 8; // consecutive windows rolled by one thread
+
 struct WinArgs {
     const uint8_t* seqs;
     const uint64_t* seg_off;   // n_segs+1 byte offsets into seqs
-    const uint64_t* seg_wbase; // n_segs+1 window prefix (this pass's range)
+    const uint64_t* seg_rbase; // n_segs+1 prefix of runs (kBRun windows) per segment
     const uint32_t* seg_doc;   // document of each segment
     const uint64_t* doc_start; // byte offset of each document's first segment
     uint64_t seg_lo, seg_hi;   // segment range of this pass
-    uint64_t w_lo, w_hi;       // window range of this pass
+    uint64_t r_lo, r_hi;       // run range of this pass
     uint32_t q, k;
     int canonical;
 };
 
-// window g -> (segment, offset in segment)
+// run g -> segment (seg_rbase[s] <= g < seg_rbase[s+1])
 __device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
-    uint64_t lo = a.seg_lo, hi = a.seg_hi; // seg_wbase[lo] <= g < seg_wbase[hi]
+    uint64_t lo = a.seg_lo, hi = a.seg_hi;
     while (hi - lo > 1) {
         uint64_t mid = (lo + hi) >> 1;
-        if (a.seg_wbase[mid] <= g)
+        if (a.seg_rbase[mid] <= g)
             lo = mid;
         else
             hi = mid;
@@ -57,40 +59,67 @@ __device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
     return lo;
 }
 
+// Calls f(j, dna, code) for the windows [j0, j1) of segment bytes `sb`
+// (dna: all-ACGT window with q <= 32, code: its canonical/forward code).
+template <int QC, typename F>
+__device__ __forceinline__ void roll_windows(const uint8_t* sb, uint64_t j0, uint64_t j1, uint32_t q_rt,
+                                             bool canonical, F&& f) {
+    const uint32_t q = QC ? QC : q_rt;
+    if (q <= 32) {
+        Roller R(q);
+        for (uint32_t i = 0; i + 1 < q; ++i) R.push(__ldg(sb + j0 + i));
+        for (uint64_t j = j0; j < j1; ++j) {
+            R.push(__ldg(sb + j + q - 1));
+            f(j, R.dna(), canonical ? R.canon() : R.fwd);
+        }
+    } else {
+        for (uint64_t j = j0; j < j1; ++j) f(j, false, 0ull);
+    }
+}
+
+template <int QC>
 __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long long* tab,
                                                     const uint64_t* tab_off, const uint64_t* tab_slots,
                                                     unsigned long long* term_count) {
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t q = QC ? QC : a.q;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t base = a.w_lo + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32;
-         base < a.w_hi; base += warps * 32) {
-        uint64_t g = base + lane;
-        bool rep = false;
-        uint32_t doc = 0;
-        if (g < a.w_hi) {
-            uint64_t s = find_seg(a, g);
+    for (uint64_t base = a.r_lo + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32;
+         base < a.r_hi; base += warps * 32) {
+        const uint64_t g = base + lane;
+        uint32_t cnt = 0, doc = 0xffffffffu;
+        if (g < a.r_hi) {
+            const uint64_t s = find_seg(a, g);
             doc = a.seg_doc[s];
-            uint64_t pos = a.seg_off[s] + (g - a.seg_wbase[s]); // byte of window start
+            const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
+            const uint64_t W = len >= q ? len - q + 1 : 0;
+            const uint64_t j0 = (g - a.seg_rbase[s]) * kBRun;
+            const uint64_t j1 = min(W, j0 + kBRun);
+            const uint8_t* sb = a.seqs + a.seg_off[s];
             const uint8_t* dbase = a.seqs + a.doc_start[doc];
-            const uint8_t* w = a.seqs + pos;
-            bool valid = true, rc = false;
-            if (a.canonical) {
-                valid = window_acgt(w, a.q);
-                if (valid) rc = choose_rc(w, a.q);
-            }
-            if (valid) {
-                uint64_t h = xxh64_term(w, a.q, rc, 0);
-                rep = set_insert(tab + tab_off[doc], tab_slots[doc] - 1, h,
-                                 static_cast<uint32_t>(pos - a.doc_start[doc]), dbase, a.q,
-                                 a.canonical != 0, rc);
-            }
+            unsigned long long* t = tab + tab_off[doc];
+            const uint64_t mask = tab_slots[doc] - 1;
+            roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
+                const uint8_t* w = sb + j;
+                const uint32_t pos = static_cast<uint32_t>(w - dbase);
+                if (dna) {
+                    cnt += set_insert_code(t, mask, xxh64_code<QC>(code, q, 0), code);
+                } else if (a.canonical) {
+                    if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
+                    const bool rc = choose_rc(w, q);
+                    cnt += set_insert(t, mask, xxh64_term(w, q, rc, 0), pos, dbase, q, true, rc);
+                } else {
+                    const uint64_t h = xxh64_term(w, q, false, 0);
+                    cnt += q <= 32 ? set_insert_tagged(t, mask, h, pos, dbase, q)
+                                   : set_insert(t, mask, h, pos, dbase, q, false, false);
+                }
+            });
         }
-        unsigned act = __ballot_sync(0xffffffffu, rep);
-        if (rep) {
-            unsigned peers = __match_any_sync(act, doc);
-            if (lane == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(term_count + doc, (unsigned long long)__popc(peers));
-        }
+        // one atomic per (warp, document)
+        const unsigned peers = __match_any_sync(0xffffffffu, doc);
+        const uint32_t sum = __reduce_add_sync(peers, cnt);
+        if (g < a.r_hi && sum && lane == (uint32_t)(__ffs(peers) - 1))
+            atomicAdd(term_count + doc, (unsigned long long)sum);
     }
 }
 
@@ -99,26 +128,39 @@ struct FillBlock {
     uint64_t w, magic, rb; // rb: row stride (the device pitch)
 };
 
+template <int QC>
 __global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* blocks,
                                                    const uint32_t* doc_block, const uint32_t* doc_col,
                                                    unsigned int* words) {
-    for (uint64_t g = a.w_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < a.w_hi;
+    const uint32_t q = QC ? QC : a.q;
+    for (uint64_t g = a.r_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < a.r_hi;
          g += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t s = find_seg(a, g);
-        uint32_t doc = a.seg_doc[s];
-        const uint8_t* w = a.seqs + a.seg_off[s] + (g - a.seg_wbase[s]);
-        bool rc = false;
-        if (a.canonical) {
-            if (!window_acgt(w, a.q)) continue;
-            rc = choose_rc(w, a.q);
-        }
+        const uint64_t s = find_seg(a, g);
+        const uint32_t doc = a.seg_doc[s];
+        const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
+        const uint64_t W = len >= q ? len - q + 1 : 0;
+        const uint64_t j0 = (g - a.seg_rbase[s]) * kBRun;
+        const uint64_t j1 = min(W, j0 + kBRun);
+        const uint8_t* sb = a.seqs + a.seg_off[s];
         const FillBlock B = blocks[doc_block[doc]];
         const uint32_t col = doc_col[doc];
-        for (uint32_t seed = 0; seed < a.k; ++seed) {
-            uint64_t r = fastmod(xxh64_term(w, a.q, rc, seed), B.w, B.magic);
-            uint64_t byte = B.base + r * B.rb + (col >> 3);
+        const uint64_t colbyte = B.base + (col >> 3);
+        auto set_bit = [&](uint64_t h) { // bit (h % w, col): bit_matrix.hpp:25-27
+            const uint64_t byte = colbyte + fastmod(h, B.w, B.magic) * B.rb;
             atomicOr(words + (byte >> 2), 1u << (((byte & 3) << 3) + (col & 7)));
-        }
+        };
+        roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
+            const uint8_t* w = sb + j;
+            if (dna) {
+                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_code<QC>(code, q, seed));
+            } else if (a.canonical) {
+                if (q <= 32 || !window_acgt(w, q)) return;
+                const bool rc = choose_rc(w, q);
+                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_term(w, q, rc, seed));
+            } else {
+                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_term(w, q, false, seed));
+            }
+        });
     }
 }
 
@@ -172,7 +214,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     } sg{st};
 
     // windows per segment / document
-    std::vector<uint64_t> seg_wbase(n_segs + 1, 0), doc_start(n_docs), doc_w(n_docs, 0);
+    std::vector<uint64_t> seg_rbase(n_segs + 1, 0), doc_start(n_docs), doc_w(n_docs, 0);
     std::vector<uint32_t> seg_doc(n_segs);
     for (uint64_t d = 0; d < n_docs; ++d) {
         doc_start[d] = n_segs ? seg_off[doc_segs[d]] : 0;
@@ -180,14 +222,14 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             seg_doc[s] = static_cast<uint32_t>(d);
             uint64_t len = seg_off[s + 1] - seg_off[s];
             uint64_t W = len >= q ? len - q + 1 : 0;
-            seg_wbase[s + 1] = seg_wbase[s] + W;
+            seg_rbase[s + 1] = seg_rbase[s] + (W + kBRun - 1) / kBRun;
             doc_w[d] += W;
         }
         if (seg_off[doc_segs[d + 1]] - doc_start[d] >= 0xffffffffull)
             throw UsageError("build: documents larger than 4 GiB are not supported");
     }
     const uint64_t total_bytes = n_segs ? seg_off[n_segs] : 0;
-    const uint64_t total_w = seg_wbase[n_segs];
+    const uint64_t total_runs = seg_rbase[n_segs];
 
     DevBuf d_seqs, d_segoff, d_segw, d_segdoc, d_docstart, d_tab, d_taboff, d_tabslots, d_tc;
     if (!seqs_on_device) d_seqs.reserve(std::max<uint64_t>(total_bytes, 1));
@@ -200,7 +242,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     if (!seqs_on_device)
         COBS_CUDA(cudaMemcpyAsync(d_seqs.ptr, seqs, total_bytes, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_segoff.ptr, seg_off, 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
-    COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_wbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_rbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     if (n_segs)
         COBS_CUDA(cudaMemcpyAsync(d_segdoc.ptr, seg_doc.data(), 4 * n_segs, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_docstart.ptr, doc_start.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
@@ -211,7 +253,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     WinArgs wa{};
     wa.seqs = seqs_on_device ? seqs : d_seqs.as<uint8_t>();
     wa.seg_off = d_segoff.as<uint64_t>();
-    wa.seg_wbase = d_segw.as<uint64_t>();
+    wa.seg_rbase = d_segw.as<uint64_t>();
     wa.seg_doc = d_segdoc.as<uint32_t>();
     wa.doc_start = d_docstart.as<uint64_t>();
     wa.q = q;
@@ -226,7 +268,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
 
     // ---- count pass, in document chunks bounded by set memory ----------
     std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
-    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(2 * doc_w[d]);
+    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] + doc_w[d] / 2 + 1);
     size_t free_b = 0, total_b = 0;
     COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t budget_slots = std::max<uint64_t>((free_b / 3) / 8, 1ull << 20);
@@ -248,13 +290,13 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
         wa.seg_lo = doc_segs[d0];
         wa.seg_hi = doc_segs[d1];
-        wa.w_lo = seg_wbase[wa.seg_lo];
-        wa.w_hi = seg_wbase[wa.seg_hi];
-        if (wa.w_hi > wa.w_lo) {
+        wa.r_lo = seg_rbase[wa.seg_lo];
+        wa.r_hi = seg_rbase[wa.seg_hi];
+        if (wa.r_hi > wa.r_lo) {
             // tab_off of the chunk's documents is relative to the chunk's tables
-            count_kernel<<<148 * 8, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(),
-                                                  d_taboff.as<uint64_t>(), d_tabslots.as<uint64_t>(),
-                                                  d_tc.as<unsigned long long>());
+            auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
+            ck<<<148 * 8, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
+                                        d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
             COBS_CUDA(cudaGetLastError());
         }
         COBS_CUDA(cudaEventRecord(e1, st));
@@ -326,10 +368,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     COBS_CUDA(cudaEventRecord(e2, st));
     wa.seg_lo = 0;
     wa.seg_hi = n_segs;
-    wa.w_lo = 0;
-    wa.w_hi = total_w;
-    if (total_w > 0) {
-        fill_kernel<<<148 * 16, 256, 0, st>>>(wa, d_fb.as<FillBlock>(), d_dblock.as<uint32_t>(),
+    wa.r_lo = 0;
+    wa.r_hi = total_runs;
+    if (total_runs > 0) {
+        auto fk = q == 31 ? fill_kernel<31> : fill_kernel<0>;
+        fk<<<148 * 16, 256, 0, st>>>(wa, d_fb.as<FillBlock>(), d_dblock.as<uint32_t>(),
                                               d_dcol.as<uint32_t>(),
                                               reinterpret_cast<unsigned int*>(ix->payload));
         COBS_CUDA(cudaGetLastError());

@@ -170,3 +170,152 @@ __device__ __forceinline__ bool set_insert(unsigned long long* tab, uint64_t mas
 }
 
 } // namespace cobsg
+
+namespace cobsg {
+
+// ---- DNA fast path: 2-bit codes ---------------------------------------
+//
+// For windows of only A/C/G/T bytes and q <= 32 the term is carried as a
+// 2q-bit code (A=0 < C=1 < G=2 < T=3, first base most significant), so
+//   * integer order of codes == bytewise order of the ASCII terms, which makes
+//     the canonical min(gram, revcomp) (termizer.cpp:117-118) a 64-bit min;
+//   * the code is an exact (injective) dedup key -- no byte compares;
+//   * forward and reverse-complement codes roll in O(1) per window;
+//   * the ASCII bytes XXH64 needs are rebuilt from the code in registers with
+//     one PRMT per 4 bases.
+// Windows with any other byte take the byte path above.
+
+// 1 iff c is one of 'A','C','G','T': all four lie in 0x40..0x5f at bit
+// positions 1, 3, 7 and 20 of the low 5 bits.
+__device__ __forceinline__ uint32_t acgt_bit(uint32_t c) {
+    return ((c & 0xe0u) == 0x40u) ? (0x10008au >> (c & 31u)) & 1u : 0u;
+}
+// 2-bit code of an A/C/G/T byte: ((c >> 1) ^ (c >> 2)) & 3 maps A,C,G,T to 0..3.
+__device__ __forceinline__ uint32_t base_code(uint32_t c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
+
+// ASCII of 4 bases given as 8 code bits (first base in bits 7..6), as a
+// little-endian word: PRMT with nibble selectors = the 2-bit codes.
+__device__ __forceinline__ uint32_t bases4_ascii(uint32_t b8) {
+    uint32_t sel = (b8 >> 6) | (b8 & 0x30u) | ((b8 & 0x0cu) << 6) | ((b8 & 0x03u) << 12);
+    return __byte_perm(0x54474341u, 0u, sel);
+}
+
+// ASCII word of bases [i, i+4) of a q-base code (i + 4 <= q).
+__device__ __forceinline__ uint32_t code_word(uint64_t code, uint32_t q, uint32_t i) {
+    return bases4_ascii(static_cast<uint32_t>(code >> (2 * (q - 4 - i))) & 0xffu);
+}
+__device__ __forceinline__ uint32_t code_byte(uint64_t code, uint32_t q, uint32_t i) {
+    return __byte_perm(0x54474341u, 0u, static_cast<uint32_t>(code >> (2 * (q - 1 - i))) & 3u) & 0xffu;
+}
+__device__ __forceinline__ uint64_t code_lane64(uint64_t code, uint32_t q, uint32_t i) {
+    return static_cast<uint64_t>(code_word(code, q, i)) |
+           (static_cast<uint64_t>(code_word(code, q, i + 4)) << 32);
+}
+
+// XXH64 of the ASCII bytes of a q-base code, 1 <= q <= 32 (QC = q when known
+// at compile time, else 0).  Same arithmetic as xxh64_term / xxhash64.hpp:45-95.
+template <int QC>
+__device__ __forceinline__ uint64_t xxh64_code(uint64_t code, uint32_t q_rt, uint64_t seed) {
+    using namespace xx;
+    const uint32_t q = QC ? QC : q_rt;
+    uint32_t i = 0;
+    uint64_t h;
+    if (q == 32) { // one 32-byte stripe
+        uint64_t v1 = rnd(seed + P1 + P2, code_lane64(code, q, 0));
+        uint64_t v2 = rnd(seed + P2, code_lane64(code, q, 8));
+        uint64_t v3 = rnd(seed, code_lane64(code, q, 16));
+        uint64_t v4 = rnd(seed - P1, code_lane64(code, q, 24));
+        h = rotl(v1, 1) + rotl(v2, 7) + rotl(v3, 12) + rotl(v4, 18);
+        h = (h ^ rnd(0, v1)) * P1 + P4;
+        h = (h ^ rnd(0, v2)) * P1 + P4;
+        h = (h ^ rnd(0, v3)) * P1 + P4;
+        h = (h ^ rnd(0, v4)) * P1 + P4;
+        i = 32;
+    } else {
+        h = seed + P5;
+    }
+    h += q;
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+        if (i + 8 <= q) {
+            h = rotl(h ^ rnd(0, code_lane64(code, q, i)), 27) * P1 + P4;
+            i += 8;
+        }
+    if (i + 4 <= q) {
+        h = rotl(h ^ ((uint64_t)code_word(code, q, i) * P1), 23) * P2 + P3;
+        i += 4;
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+        if (i < q) {
+            h = rotl(h ^ ((uint64_t)code_byte(code, q, i) * P5), 11) * P1;
+            ++i;
+        }
+    h ^= h >> 33;
+    h *= P2;
+    h ^= h >> 29;
+    h *= P3;
+    h ^= h >> 32;
+    return h;
+}
+
+// Rolling 2-bit codes over a run of windows.  push() consumes one byte;
+// after q pushes without a non-ACGT byte in the last q, fwd/rev hold the
+// window's forward and reverse-complement codes.
+struct Roller {
+    uint64_t fwd = 0, rev = 0, mask;
+    uint32_t q, since_bad; // bytes since the last non-ACGT byte
+    __device__ explicit Roller(uint32_t q_) : mask(q_ >= 32 ? ~0ull : ((1ull << (2 * q_)) - 1)), q(q_), since_bad(0) {}
+    __device__ __forceinline__ void push(uint32_t c) {
+        uint32_t ok = acgt_bit(c);
+        uint64_t code = base_code(c);
+        fwd = ((fwd << 2) | code) & mask;
+        rev = (rev >> 2) | ((3ull - code) << (2 * (q - 1)));
+        since_bad = ok ? since_bad + 1 : 0;
+    }
+    __device__ __forceinline__ bool dna() const { return since_bad >= q; }
+    // canonical term code: min(gram, revcomp) bytewise == min of the codes
+    __device__ __forceinline__ uint64_t canon() const { return fwd < rev ? fwd : rev; }
+};
+
+// Exact set insert keyed by the 2-bit code (bit 63 clear; +1 keeps 0 empty).
+// Byte-path keys (set_insert above) always have bit 63 set when both kinds
+// share a table (see set_insert_tagged), so the key spaces never collide.
+__device__ __forceinline__ bool set_insert_code(unsigned long long* tab, uint64_t mask, uint64_t h,
+                                                uint64_t code) {
+    const unsigned long long key = static_cast<unsigned long long>(code) + 1ull;
+    uint64_t slot = h & mask;
+    for (;;) {
+        unsigned long long cur = *((volatile unsigned long long*)&tab[slot]);
+        if (cur == 0ull) {
+            cur = atomicCAS(&tab[slot], 0ull, key);
+            if (cur == 0ull) return true;
+        }
+        if (cur == key) return false;
+        slot = (slot + 1) & mask;
+    }
+}
+
+// Byte-path insert for tables shared with code keys: key bit 63 set, 31-bit
+// hash tag, 32-bit position+1; equal tags are resolved by the window bytes.
+__device__ __forceinline__ bool set_insert_tagged(unsigned long long* tab, uint64_t mask, uint64_t h,
+                                                  uint32_t pos, const uint8_t* win_base, uint32_t q) {
+    const unsigned long long key = (1ull << 63) | ((unsigned long long)((h >> 33) & 0x7fffffffu) << 32) |
+                                   (unsigned long long)(pos + 1u);
+    uint64_t slot = h & mask;
+    const uint8_t* mine = win_base + pos;
+    for (;;) {
+        unsigned long long cur = *((volatile unsigned long long*)&tab[slot]);
+        if (cur == 0ull) {
+            cur = atomicCAS(&tab[slot], 0ull, key);
+            if (cur == 0ull) return true;
+        }
+        if ((cur >> 32) == (key >> 32)) {
+            const uint8_t* other = win_base + ((uint32_t)cur - 1u);
+            if (terms_equal(mine, false, other, false, q)) return false;
+        }
+        slot = (slot + 1) & mask;
+    }
+}
+
+} // namespace cobsg

@@ -29,16 +29,10 @@ namespace {
 #define COBS_GATHER_MINB 3
 #endif
 constexpr int kTermizeThreads = 256;
-constexpr uint32_t kSmemSlots = 8192; // 64 KB of shared set per CTA
+constexpr uint32_t kSmemSlots = 16384; // <= 128 KB of shared set per CTA
 constexpr uint64_t kNoGtab = ~0ull;
 
 inline uint64_t next_pow2(uint64_t x) {
-    uint64_t p = 2;
-    while (p < x) p <<= 1;
-    return p;
-}
-
-__device__ __forceinline__ uint64_t next_pow2_dev(uint64_t x) {
     uint64_t p = 2;
     while (p < x) p <<= 1;
     return p;
@@ -56,63 +50,182 @@ struct TermizeArgs {
     uint32_t q, k;
     int canonical;
     double K;
+    uint32_t smem_slots; // shared-memory set capacity (tile arrays follow it)
     uint64_t* hashes; // [win_total * k]
     uint32_t* ell;
     uint64_t* skipped;
     uint32_t* tau;
 };
 
+// Set size for W windows: load factor <= 2/3 (same formula on the host).
+__host__ __device__ __forceinline__ uint64_t set_slots(uint64_t W) {
+    uint64_t x = W + W / 2 + 1, p = 2;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Tile of the pattern in shared memory with per-position codes of runs of
+// 1, 2, 4, 8, 16 bases and their all-ACGT flags, built by doubling
+// (c2L[j] = cL[j] << 2L | cL[j+L]); a window's code is then 5 lookups.
+constexpr int kTile = 2048;           // windows per tile
+constexpr int kTileP = kTile + 32;    // positions per tile
+constexpr size_t kTileBytes = (size_t)kTileP * (4 + 2 + 1 + 1 + 1) + (size_t)kTileP * 5;
+
+struct TileView {
+    uint32_t* c16;
+    uint16_t* c8;
+    uint8_t *c4, *c2, *c1;
+    uint8_t* ok[5]; // ok[b][j]: bases [j, j + 2^b) are all A/C/G/T
+    __device__ explicit TileView(uint8_t* base) {
+        c16 = reinterpret_cast<uint32_t*>(base);
+        c8 = reinterpret_cast<uint16_t*>(c16 + kTileP);
+        c4 = reinterpret_cast<uint8_t*>(c8 + kTileP);
+        c2 = c4 + kTileP;
+        c1 = c2 + kTileP;
+        for (int b = 0; b < 5; ++b) ok[b] = c1 + kTileP * (b + 1);
+    }
+    // code and validity of the q-base window at tile position j (q <= 32)
+    __device__ __forceinline__ uint64_t window(uint32_t j, uint32_t q, bool& valid) const {
+        uint64_t code = 0;
+        uint32_t off = j, good = 1;
+        if (q & 32) {
+            code = (static_cast<uint64_t>(c16[off]) << 32) | c16[off + 16];
+            good = ok[4][off] & ok[4][off + 16];
+            off += 32;
+        }
+        if (q & 16) { code = (code << 32) | c16[off]; good &= ok[4][off]; off += 16; }
+        if (q & 8) { code = (code << 16) | c8[off]; good &= ok[3][off]; off += 8; }
+        if (q & 4) { code = (code << 8) | c4[off]; good &= ok[2][off]; off += 4; }
+        if (q & 2) { code = (code << 4) | c2[off]; good &= ok[1][off]; off += 2; }
+        if (q & 1) { code = (code << 2) | c1[off]; good &= ok[0][off]; }
+        valid = good != 0;
+        return code;
+    }
+};
+
+// Reverse complement of a q-base code: complement every base (xor 3), then
+// reverse the order of the 2-bit groups.
+__device__ __forceinline__ uint64_t revcomp_code(uint64_t code, uint32_t q) {
+    uint64_t x = __brevll(~code);
+    x = ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+    return x >> (64 - 2 * q);
+}
+
+// One CTA per query.  The pattern is staged tile by tile into shared memory;
+// every thread then takes 8 consecutive windows: all-ACGT windows (q <= 32)
+// get their code from the tile (canonical = min(code, revcomp)), XXH64 from
+// the code and an exact code-keyed insert; other windows take the byte path.
+// The distinct terms are compacted in window order.  QC: 31 or 0.
+template <int QC>
 __global__ void __launch_bounds__(kTermizeThreads) termize_hash_kernel(TermizeArgs a) {
-    extern __shared__ unsigned long long s_tab[];
-    using Scan = cub::BlockScan<uint32_t, kTermizeThreads>;
+    extern __shared__ __align__(16) unsigned long long s_dyn[];
     using Reduce = cub::BlockReduce<uint64_t, kTermizeThreads>;
-    __shared__ union {
-        typename Scan::TempStorage scan;
-        typename Reduce::TempStorage reduce;
-    } tmp;
-    const uint32_t q = a.q, k = a.k;
+    __shared__ typename Reduce::TempStorage tmp_reduce;
+    __shared__ uint32_t s_count; // distinct terms of the current query
+    const uint32_t q = QC ? QC : a.q, k = a.k;
+    const bool code_path = q <= 32; // DNA windows carried as 2-bit codes
+    unsigned long long* s_tab = s_dyn;
+    TileView T(reinterpret_cast<uint8_t*>(s_dyn + a.smem_slots));
     for (uint64_t qi = blockIdx.x; qi < a.n; qi += gridDim.x) {
         const uint64_t W = a.win_base[qi + 1] - a.win_base[qi];
+        const uint64_t L = a.off[qi + 1] - a.off[qi];
         const uint8_t* pat = a.pats + a.off[qi];
-        const uint64_t S = next_pow2_dev(2 * W);
+        const uint64_t S = set_slots(W);
         unsigned long long* tab = a.tab_off[qi] == kNoGtab ? s_tab : a.gtab + a.tab_off[qi];
         for (uint64_t s = threadIdx.x; s < S; s += blockDim.x) tab[s] = 0ull;
-        __syncthreads();
         uint64_t* out = a.hashes + a.win_base[qi] * k;
-        uint64_t ell = 0, skipped = 0;
-        for (uint64_t base = 0; base < W; base += blockDim.x) {
-            uint64_t j = base + threadIdx.x;
-            uint32_t rep = 0;
-            uint64_t h0 = 0;
-            bool rc = false;
-            if (j < W) {
+        uint64_t skipped = 0;
+        if (threadIdx.x == 0) s_count = 0;
+        for (uint64_t tb = 0; tb < W; tb += kTile) {
+            __syncthreads(); // table cleared / previous tile consumed
+            const uint32_t nwin = static_cast<uint32_t>(W - tb < (uint64_t)kTile ? W - tb : (uint64_t)kTile);
+            if (code_path) {
+                // positions needed: nwin + q - 1 (rounded so every level is defined)
+                const uint32_t np = nwin + 32 < (uint32_t)kTileP ? nwin + 32 : (uint32_t)kTileP;
+                for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+                    const uint32_t c = tb + i < L ? __ldg(pat + tb + i) : 'A';
+                    T.c1[i] = static_cast<uint8_t>(base_code(c));
+                    T.ok[0][i] = static_cast<uint8_t>(acgt_bit(c));
+                }
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i + 1 < np; i += blockDim.x) {
+                    T.c2[i] = static_cast<uint8_t>((T.c1[i] << 2) | T.c1[i + 1]);
+                    T.ok[1][i] = T.ok[0][i] & T.ok[0][i + 1];
+                }
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i + 3 < np; i += blockDim.x) {
+                    T.c4[i] = static_cast<uint8_t>((T.c2[i] << 4) | T.c2[i + 2]);
+                    T.ok[2][i] = T.ok[1][i] & T.ok[1][i + 2];
+                }
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i + 7 < np; i += blockDim.x) {
+                    T.c8[i] = static_cast<uint16_t>((T.c4[i] << 8) | T.c4[i + 4]);
+                    T.ok[3][i] = T.ok[2][i] & T.ok[2][i + 4];
+                }
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i + 15 < np; i += blockDim.x) {
+                    T.c16[i] = (static_cast<uint32_t>(T.c8[i]) << 16) | T.c8[i + 8];
+                    T.ok[4][i] = T.ok[3][i] & T.ok[3][i + 8];
+                }
+                __syncthreads();
+            }
+            // window r*threads + tid: every thread busy even for short patterns;
+            // winners are appended with one shared atomic per warp and round
+            // (term order inside the list is irrelevant: scores are sums)
+            for (uint32_t r0 = 0; r0 < nwin; r0 += kTermizeThreads) {
+                const uint32_t jl = r0 + threadIdx.x;
+                const bool active = jl < nwin;
+                const uint64_t j = tb + jl;
                 const uint8_t* w = pat + j;
-                bool valid = true;
-                if (a.canonical) { // termizer.cpp:112-119
-                    valid = window_acgt(w, q);
-                    if (valid) rc = choose_rc(w, q);
+                bool won = false, bytep = false, rc = false;
+                uint64_t h = 0, code = 0;
+                if (active) {
+                    bool dna = false;
+                    if (code_path) code = T.window(jl, q, dna);
+                    if (dna) {
+                        if (a.canonical) { // termizer.cpp:117-119: min(gram, revcomp)
+                            const uint64_t rcc = revcomp_code(code, q);
+                            code = rcc < code ? rcc : code;
+                        }
+                        h = xxh64_code<QC>(code, q, 0);
+                        won = set_insert_code(tab, S - 1, h, code);
+                    } else if (a.canonical) {
+                        // non-ACGT window: skipped (termizer.cpp:113-116); for q > 32
+                        // the ACGT windows take the canonical byte path
+                        if (code_path || !window_acgt(w, q)) {
+                            ++skipped;
+                        } else {
+                            rc = choose_rc(w, q);
+                            h = xxh64_term(w, q, rc, 0);
+                            bytep = true;
+                            won = set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, true, rc);
+                        }
+                    } else { // raw bytes (any alphabet): termizer.cpp:120-122
+                        h = xxh64_term(w, q, false, 0);
+                        bytep = true;
+                        won = code_path
+                                  ? set_insert_tagged(tab, S - 1, h, static_cast<uint32_t>(j), pat, q)
+                                  : set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, false, false);
+                    }
                 }
-                if (!valid) {
-                    ++skipped;
-                } else {
-                    h0 = xxh64_term(w, q, rc, 0);
-                    rep = set_insert(tab, S - 1, h0, static_cast<uint32_t>(j), pat, q,
-                                     a.canonical != 0, rc)
-                              ? 1u
-                              : 0u;
+                const unsigned m = __ballot_sync(0xffffffffu, won);
+                if (m) {
+                    const uint32_t lane = threadIdx.x & 31u;
+                    uint32_t base = 0;
+                    if (lane == 0) base = atomicAdd(&s_count, static_cast<uint32_t>(__popc(m)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (won) { // seed-major per term: query.cpp:141-144
+                        uint64_t* dst = out + static_cast<uint64_t>(base + __popc(m & ((1u << lane) - 1u))) * k;
+                        dst[0] = h;
+                        for (uint32_t s = 1; s < k; ++s)
+                            dst[s] = bytep ? xxh64_term(w, q, rc, s) : xxh64_code<QC>(code, q, s);
+                    }
                 }
             }
-            uint32_t excl, total;
-            Scan(tmp.scan).ExclusiveSum(rep, excl, total);
-            if (rep) { // seed-major per term: query.cpp:141-144
-                uint64_t* dst = out + (ell + excl) * k;
-                dst[0] = h0;
-                for (uint32_t s = 1; s < k; ++s) dst[s] = xxh64_term(pat + j, q, rc, s);
-            }
-            ell += total;
-            __syncthreads();
         }
-        uint64_t skip_total = Reduce(tmp.reduce).Sum(skipped);
+        __syncthreads();
+        const uint64_t ell = s_count;
+        uint64_t skip_total = Reduce(tmp_reduce).Sum(skipped);
         if (threadIdx.x == 0) {
             a.ell[qi] = static_cast<uint32_t>(ell);
             a.skipped[qi] = skip_total;
@@ -506,7 +619,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
         if (W >= 0xffffffffull) throw UsageError("query: pattern longer than 2^32-2 grams");
         win_base[i + 1] = win_base[i] + W;
         wmax = std::max(wmax, W);
-        uint64_t S = next_pow2(2 * W);
+        uint64_t S = set_slots(W);
         if (S <= kSmemSlots) {
             tab_off[i] = kNoGtab;
         } else {
@@ -572,12 +685,14 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ta.tau = ws.tau.as<uint32_t>();
     uint64_t small_S = 2;
     for (uint64_t i = 0; i < n; ++i)
-        if (tab_off[i] == kNoGtab) small_S = std::max(small_S, next_pow2(2 * (win_base[i + 1] - win_base[i])));
-    size_t smem = static_cast<size_t>(std::min<uint64_t>(small_S, kSmemSlots)) * 8;
-    COBS_CUDA(cudaFuncSetAttribute(termize_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (tab_off[i] == kNoGtab) small_S = std::max(small_S, set_slots(win_base[i + 1] - win_base[i]));
+    ta.smem_slots = static_cast<uint32_t>(std::min<uint64_t>(small_S, kSmemSlots));
+    size_t smem = static_cast<size_t>(ta.smem_slots) * 8 + kTileBytes;
+    auto k1 = q == 31 ? termize_hash_kernel<31> : termize_hash_kernel<0>;
+    COBS_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     unsigned grid1 = static_cast<unsigned>(std::min<uint64_t>(n, 1u << 30));
-    termize_hash_kernel<<<grid1, kTermizeThreads, smem, st>>>(ta);
+    k1<<<grid1, kTermizeThreads, smem, st>>>(ta);
     COBS_CUDA(cudaGetLastError());
     R.launches += 1;
     COBS_CUDA(cudaEventRecord(ev[1], st));
