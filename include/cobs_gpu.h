@@ -187,6 +187,15 @@ int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t
                       uint32_t flags, const char* out_path, uint8_t** image, uint64_t* image_len,
                       cobs_gpu_index** index_out, char* err, size_t errlen);
 
+/* Replaces cobs::merge_classic (proj/include/cobs/classic_index.hpp:46-49,
+ * proj/src/classic_index.cpp:96-115): documents of `a` then `b`, every row the
+ * bit-concatenation of a's and b's (bit_matrix.cpp:10-23), computed on the
+ * device into a new device-resident index.  COBS_EDATA on differing
+ * parameters / widths or duplicate names (same messages); COBS_EUSAGE unless
+ * both are classic and resident on `device`. */
+int cobs_gpu_merge_classic(const cobs_gpu_index* a, const cobs_gpu_index* b, int device,
+                           cobs_gpu_index** out, char* err, size_t errlen);
+
 /* Build timings (ms) of the calling thread's last cobs_gpu_build: term
  * counting, fill (sequences in HBM -> finished matrix), total incl. H2D,
  * D2H and serialisation. */

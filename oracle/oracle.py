@@ -290,6 +290,9 @@ def ref():
                                       C.c_double, C.c_int, _u64, C.c_int, _u64, C.c_uint32,
                                       C.c_char_p, C.c_char_p, C.c_size_t]
         L.ref_open.argtypes = [C.c_char_p, C.POINTER(_vp), C.c_char_p, C.c_size_t]
+        L.ref_merge_write.argtypes = [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_uint32,
+                                      C.c_uint32, C.c_double, C.c_int, _u64, C.c_char_p, C.c_char_p,
+                                      C.c_size_t]
         L.ref_c5_open.argtypes = [_u64, _u64, _u64, C.c_double, C.c_double, C.c_double, C.c_int,
                                   C.c_int, C.POINTER(_vp), C.c_char_p, C.c_size_t]
         L.ref_close.argtypes = [_vp]
@@ -411,3 +414,21 @@ def ref_extract_terms(content: Sequence[bytes], q: int, canonical: bool):
     raw = _take(terms, ell.value * q)
     ref().ref_free(terms)
     return [raw[i * q:(i + 1) * q] for i in range(ell.value)], sk.value, occ.value
+
+
+def ref_merge_write(docs, split: int, path: str, forced_w: int, q=31, k=1, p=0.3, canonical=False):
+    """The reference's merge_classic of docs[:split] and docs[split:] built at
+    a common forced width, written by its write_index."""
+    segs, doc_seg, names = [], [0], []
+    for name, content in docs:
+        names.append(name)
+        segs.extend(content)
+        doc_seg.append(len(segs))
+    keep, ptrs, lens = _segs(segs)
+    ds = (C.c_uint64 * len(doc_seg))(*doc_seg)
+    nm = (C.c_char_p * max(len(names), 1))(*names)
+    err = C.create_string_buffer(1024)
+    rc = ref().ref_merge_write(ptrs, lens, ds, nm, len(names), split, q, k, p, 1 if canonical else 0,
+                               forced_w, path.encode(), err, 1024)
+    if rc:
+        raise OracleError(rc, err.value.decode())

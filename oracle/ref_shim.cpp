@@ -235,6 +235,31 @@ int ref_build_write(const uint8_t* const* segs, const uint64_t* lens, const uint
     });
 }
 
+// build_classic over docs [0, split) and [split, n) with a common forced
+// width, merge_classic, write_index (acceptance.cpp criterion 9 shape).
+int ref_merge_write(const uint8_t* const* segs, const uint64_t* lens, const uint64_t* doc_seg,
+                    const char* const* names, size_t n_docs, size_t split, uint32_t q, uint32_t k,
+                    double p, int canonical, uint64_t forced_w, const char* path, char* err,
+                    size_t errlen) {
+    return guarded(err, errlen, [&] {
+        cobs::IndexParams params;
+        params.q = q;
+        params.k = k;
+        params.p = p;
+        params.canonical = canonical != 0;
+        std::vector<cobs::TermSet> left, right;
+        for (size_t d = 0; d < n_docs; ++d) {
+            std::vector<std::string> content;
+            for (uint64_t s = doc_seg[d]; s < doc_seg[d + 1]; ++s)
+                content.emplace_back(reinterpret_cast<const char*>(segs[s]), lens[s]);
+            (d < split ? left : right).push_back(cobs::extract_terms(names[d], content, q, canonical != 0));
+        }
+        cobs::ClassicIndex a = cobs::build_classic(left, params, 1, forced_w);
+        cobs::ClassicIndex b = cobs::build_classic(right, params, 1, forced_w);
+        cobs::write_index(cobs::merge_classic(a, b), path);
+    });
+}
+
 int ref_open(const char* path, void** out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         auto h = std::make_unique<Handle>();

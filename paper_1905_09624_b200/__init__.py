@@ -452,6 +452,16 @@ def synth_docs_device(seed: int, alpha: int, lengths: np.ndarray, dev_ptr: int, 
         raise CudaError("synth_docs failed")
 
 
+def merge_classic(a: DeviceIndexView, b: DeviceIndexView, device: int = 0) -> DeviceIndexView:
+    """merge_classic (classic_index.hpp:46-49) on the device."""
+    h = C.c_void_p()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_merge_classic(a._h, b._h, device, C.byref(h), err, len(err))
+    if rc:
+        _raise(rc, err)
+    return DeviceIndexView(h.value)
+
+
 def last_build_timing() -> Tuple[float, float, float]:
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     N.lib.cobs_gpu_build_timing(C.byref(a), C.byref(b), C.byref(c))

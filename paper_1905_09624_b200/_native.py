@@ -86,6 +86,7 @@ SIGNATURES = {
                                     C.POINTER(IndexParamsC), C.c_int, C.c_uint64, C.c_int,
                                     C.c_uint32, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_uint64),
                                     C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    "cobs_gpu_merge_classic": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_build_timing": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]),
     "cobs_gpu_free": (None, [vp]),

@@ -9,6 +9,7 @@
 #include "../../include/cobs_gpu.h"
 #include "build.hpp"
 #include "index.hpp"
+#include "merge.hpp"
 
 struct cobs_gpu_index {
     std::unique_ptr<cobsg::DeviceIndex> ix;
@@ -296,6 +297,16 @@ int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_
                    size_t errlen) {
     return cobs_gpu_build_ex(seqs, seg_offsets, n_segs, doc_segs, names, n_docs, params, kind,
                              forced_w, device, 0, out_path, image, image_len, nullptr, err, errlen);
+}
+
+int cobs_gpu_merge_classic(const cobs_gpu_index* a, const cobs_gpu_index* b, int device,
+                           cobs_gpu_index** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::merge_classic(*a->ix, *b->ix, device);
+        *out = h.release();
+    });
 }
 
 int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total) {

@@ -235,3 +235,50 @@ def test_build_device_resident(gpu):
     ell, sk, st, nh, dense = idx.query_batch(qb, qo, 1e-12, scores=True)
     assert np.array_equal(got.dense.astype(np.uint32), dense)
     view.close()
+
+
+@pytest.mark.parametrize("split", [35, 32])
+def test_merge_classic(gpu, tmp_path, split):
+    """acceptance.cpp criterion 9 on the device: merge of two forced-width
+    builds == the single build, byte for byte, == the reference's merge."""
+    rng = random.Random(4444 + split)
+    docs = [(b"doc%04d" % i, [rand(rng, rng.randint(100, 8000))]) for i in range(60)]
+    whole = cb.build_classic(docs, device=gpu)
+    w = O.OracleIndex.parse(whole).blocks()[0][1]
+    va, _ = cb.build_device(*_packed(docs[:split]), cb.IndexParams(), cb.KIND_CLASSIC, forced_w=w)
+    vb, _ = cb.build_device(*_packed(docs[split:]), cb.IndexParams(), cb.KIND_CLASSIC, forced_w=w)
+    merged = cb.merge_classic(va, vb)
+    img = cb.index_image(merged)
+    assert img == whole
+    if O.ref_available():
+        path = str(tmp_path / "m.cobs")
+        O.ref_merge_write(docs, split, path, w)
+        assert open(path, "rb").read() == img
+    pats = [docs[i][1][0][:200] for i in range(0, 60, 7)]
+    x = cb.query_batch(merged, pats, 0.7)
+    y = O.OracleIndex.parse(whole)
+    for i, p in enumerate(pats):
+        ell, sk, hits, _ = y.query(p, 0.7)
+        assert gpu_hits(merged, x, i) == [list(h) for h in hits]
+    # error taxonomy of classic_index.cpp:96-106
+    vc, _ = cb.build_device(*_packed(docs[split:]), cb.IndexParams(), cb.KIND_CLASSIC, forced_w=w + 1)
+    with pytest.raises(cb.DataError, match=r"merge: widths differ \(%d vs %d\)" % (w, w + 1)):
+        cb.merge_classic(va, vc)
+    vd, _ = cb.build_device(*_packed(docs[split:]), cb.IndexParams(k=2), cb.KIND_CLASSIC, forced_w=w)
+    with pytest.raises(cb.DataError, match="merge: index parameters differ"):
+        cb.merge_classic(va, vd)
+    with pytest.raises(cb.DataError, match="duplicate document name: doc0000"):
+        cb.merge_classic(va, va)
+    for v in (va, vb, vc, vd, merged):
+        v.close()
+
+
+def _packed(docs):
+    names = [d[0] for d in docs]
+    segs = [s for d in docs for s in d[1]]
+    off = np.zeros(len(segs) + 1, np.uint64)
+    np.cumsum([len(s) for s in segs], out=off[1:])
+    doc_segs = np.zeros(len(docs) + 1, np.uint64)
+    np.cumsum([len(d[1]) for d in docs], out=doc_segs[1:])
+    buf = np.frombuffer(b"".join(segs), np.uint8) if segs else np.zeros(1, np.uint8)
+    return buf, off, doc_segs, names
