@@ -6,7 +6,8 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            -Xcudafe --diag_suppress=177
 SRC := paper_1905_09624_b200/csrc
 OUT := paper_1905_09624_b200/_lib
-OBJS := $(OUT)/host.o $(OUT)/index.o $(OUT)/query.o $(OUT)/build.o $(OUT)/merge.o $(OUT)/capi.o
+OBJS := $(OUT)/host.o $(OUT)/frontend.o $(OUT)/index.o $(OUT)/query.o $(OUT)/build.o $(OUT)/merge.o \
+        $(OUT)/capi.o
 HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh $(SRC)/*.h) include/cobs_gpu.h
 
 .PHONY: all lib oracle clean
@@ -24,6 +25,10 @@ $(OUT)/%.o: $(SRC)/%.cu $(HDRS)
 $(OUT)/host.o: $(SRC)/host.cpp $(HDRS)
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
+
+$(OUT)/frontend.o: $(SRC)/frontend.cpp $(HDRS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(OUT)/capi.o: $(SRC)/capi.cpp $(HDRS)
 	@mkdir -p $(OUT)

@@ -203,6 +203,33 @@ int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total);
 
 void cobs_gpu_free(void* p);
 
+/* ---- file front ends ------------------------------ */
+
+#define COBS_FORMAT_AUTO 0  /* by extension: .fa/.fasta/.fna -> FASTA, else text */
+#define COBS_FORMAT_FASTA 1
+#define COBS_FORMAT_TEXT 2
+
+/* `cobs query index -F queries.fa -K K -t top_t` (proj/src/cli.cpp:192-223):
+ * FASTA records read as read_fasta_named does (termizer.cpp:150-162:
+ * uppercased sequence lines, name = header up to the first blank,
+ * "query_<N>" for empty headers), queried as one batch, and the CLI's batch
+ * output returned byte for byte: per record "*name	N
+" then N lines
+ * "doc	score	ell
+", or "*name	ERR	<message>
+" (cli.cpp:187-190,214-218).
+ * *tsv is NUL-terminated; free with cobs_gpu_free. */
+int cobs_gpu_query_fasta(cobs_gpu_index* index, const char* fasta_path, double K, uint64_t top_t,
+                         char** tsv, uint64_t* tsv_len, char* err, size_t errlen);
+
+/* `cobs build inputs... --mode classic|compact --format F` (cli.cpp:112-166):
+ * directories expand recursively in lexicographic path order, every file is
+ * one document named by its stem (load_document, termizer.cpp:168-172),
+ * FASTA records are separate content strings.  Output as cobs_gpu_build. */
+int cobs_gpu_build_files(const char* const* inputs, uint64_t n_inputs, const cobs_index_params* params,
+                         int kind, int format, int device, const char* out_path, uint8_t** image,
+                         uint64_t* image_len, char* err, size_t errlen);
+
 /* ---- synthetic workloads (bench / tests; not part of the reference
  *      boundary) ----------------------------------------------------- */
 

@@ -290,6 +290,11 @@ def ref():
                                       C.c_double, C.c_int, _u64, C.c_int, _u64, C.c_uint32,
                                       C.c_char_p, C.c_char_p, C.c_size_t]
         L.ref_open.argtypes = [C.c_char_p, C.POINTER(_vp), C.c_char_p, C.c_size_t]
+        L.ref_query_fasta_tsv.argtypes = [_vp, C.c_char_p, C.c_double, _u64, C.POINTER(_vp),
+                                          C.c_char_p, C.c_size_t]
+        L.ref_build_files.argtypes = [C.POINTER(C.c_char_p), C.c_size_t, C.c_uint32, C.c_uint32,
+                                      C.c_double, C.c_int, _u64, C.c_int, C.c_int, C.c_char_p,
+                                      C.c_char_p, C.c_size_t]
         L.ref_merge_write.argtypes = [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_uint32,
                                       C.c_uint32, C.c_double, C.c_int, _u64, C.c_char_p, C.c_char_p,
                                       C.c_size_t]
@@ -333,6 +338,17 @@ class RefIndex:
         if rc:
             raise OracleError(rc, err.value.decode())
         return cls(h)
+
+    def query_fasta_tsv(self, path: str, K: float, top_t: int = 0) -> bytes:
+        out = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = ref().ref_query_fasta_tsv(self.h, path.encode(), K, top_t, C.byref(out), err, 1024)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        try:
+            return C.string_at(out)
+        finally:
+            ref().ref_free(out)
 
     def close(self):
         if self.h:
@@ -430,5 +446,15 @@ def ref_merge_write(docs, split: int, path: str, forced_w: int, q=31, k=1, p=0.3
     err = C.create_string_buffer(1024)
     rc = ref().ref_merge_write(ptrs, lens, ds, nm, len(names), split, q, k, p, 1 if canonical else 0,
                                forced_w, path.encode(), err, 1024)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+
+
+def ref_build_files(inputs, out_path: str, q=31, k=1, p=0.3, canonical=False, block_size=1024,
+                    kind=1, format=0):
+    arr = (C.c_char_p * max(len(inputs), 1))(*[str(i).encode() for i in inputs])
+    err = C.create_string_buffer(1024)
+    rc = ref().ref_build_files(arr, len(inputs), q, k, p, 1 if canonical else 0, block_size, kind,
+                               format, out_path.encode(), err, 1024)
     if rc:
         raise OracleError(rc, err.value.decode())

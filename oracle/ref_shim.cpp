@@ -14,6 +14,8 @@
 // cobs::IndexView interface (index_view.hpp:18-47), which the config-5
 // procedural/in-memory views below implement.
 #include <algorithm>
+#include <filesystem>
+#include <sstream>
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -351,6 +353,81 @@ int ref_query_batch(void* hv, const uint8_t* pats, const uint64_t* off, size_t n
     for (int i = 0; i < std::max(1, threads); ++i) th.emplace_back(work);
     for (auto& x : th) x.join();
     return 0;
+}
+
+// `cobs query idx -F file` batch output (cli.cpp:192-223, print_hits
+// :187-190), restated here because cli.cpp itself cannot be compiled (its
+// CLI11 dependency is absent): the reference's read_fasta_named + query()
+// per record, the CLI's exact formatting.  *out malloc'd.
+int ref_query_fasta_tsv(void* hv, const char* path, double K, uint64_t top_t, char** out, char* err,
+                        size_t errlen) {
+    Handle* h = static_cast<Handle*>(hv);
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        if (!(K > 0.0 && K <= 1.0)) throw std::invalid_argument("K must be in (0,1]");
+        auto queries = cobs::read_fasta_named(path);
+        std::ostringstream o;
+        for (const auto& [name, sequence] : queries) {
+            try {
+                cobs::QueryOptions opts;
+                opts.K = K;
+                opts.top_t = top_t;
+                cobs::QueryResult r = cobs::query(*h->view, sequence, opts);
+                o << '*' << name << '\t' << r.hits.size() << '\n';
+                for (const auto& hit : r.hits) o << hit.doc_name << '\t' << hit.score << '\t' << r.ell << '\n';
+            } catch (const cobs::DataError& e) {
+                o << '*' << name << "\tERR\t" << e.what() << '\n';
+            }
+        }
+        std::string s = o.str();
+        *out = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*out, s.c_str(), s.size() + 1);
+    });
+}
+
+// `cobs build inputs... --mode M --format F` (cli.cpp:112-166) with the
+// reference's load_document / build_* / write_index; expand_inputs
+// (cli.cpp:60-82) restated for the same reason as above.
+int ref_build_files(const char* const* inputs, size_t n, uint32_t q, uint32_t k, double p, int canonical,
+                    uint64_t block_size, int kind, int format, const char* out_path, char* err,
+                    size_t errlen) {
+    namespace fs = std::filesystem;
+    return guarded(err, errlen, [&] {
+        cobs::IndexParams params;
+        params.q = q;
+        params.k = k;
+        params.p = p;
+        params.canonical = canonical != 0;
+        params.block_size = block_size;
+        params.validate();
+        std::vector<fs::path> files;
+        for (size_t i = 0; i < n; ++i) {
+            fs::path path(inputs[i]);
+            std::error_code ec;
+            if (fs::is_directory(path, ec)) {
+                std::vector<fs::path> found;
+                for (const auto& e : fs::recursive_directory_iterator(path))
+                    if (e.is_regular_file()) found.push_back(e.path());
+                std::sort(found.begin(), found.end(),
+                          [](const fs::path& a, const fs::path& b) { return a.string() < b.string(); });
+                files.insert(files.end(), found.begin(), found.end());
+            } else if (fs::is_regular_file(path, ec)) {
+                files.push_back(path);
+            } else {
+                throw cobs::DataError(std::string("input not found: ") + inputs[i]);
+            }
+        }
+        if (files.empty()) throw cobs::DataError("no input files");
+        cobs::InputFormat fmt = format == 1   ? cobs::InputFormat::fasta
+                                : format == 2 ? cobs::InputFormat::text
+                                              : cobs::InputFormat::autodetect;
+        std::vector<cobs::TermSet> docs;
+        for (const auto& f : files) docs.push_back(cobs::load_document(f, q, canonical != 0, fmt));
+        if (kind == 0)
+            cobs::write_index(cobs::build_classic(docs, params, 1), out_path);
+        else
+            cobs::write_index(cobs::build_compact(docs, params, 1), out_path);
+    });
 }
 
 } // extern "C"

@@ -462,6 +462,43 @@ def merge_classic(a: DeviceIndexView, b: DeviceIndexView, device: int = 0) -> De
     return DeviceIndexView(h.value)
 
 
+FORMAT_AUTO, FORMAT_FASTA, FORMAT_TEXT = 0, 1, 2
+
+
+def query_fasta(view: DeviceIndexView, fasta_path: str, K: float = 0.9, top_t: int = 0) -> bytes:
+    """`cobs query index -F queries.fa`: the CLI's batch TSV, byte for byte."""
+    out = C.c_void_p()
+    ln = C.c_uint64()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_query_fasta(view._h, str(fasta_path).encode(), K, top_t, C.byref(out),
+                                    C.byref(ln), err, len(err))
+    if rc:
+        _raise(rc, err)
+    try:
+        return _take_bytes(out, ln.value)
+    finally:
+        N.lib.cobs_gpu_free(out)
+
+
+def build_files(inputs: Sequence[str], params: IndexParams = IndexParams(), kind: int = KIND_COMPACT,
+                format: int = FORMAT_AUTO, path: Optional[str] = None, device: int = 0) -> bytes:
+    """`cobs build inputs... --mode classic|compact`: returns the file image."""
+    arr = (C.c_char_p * max(len(inputs), 1))(*[str(i).encode() for i in inputs])
+    img = C.c_void_p()
+    ln = C.c_uint64()
+    err = _errbuf()
+    cp = params._c()
+    rc = N.lib.cobs_gpu_build_files(arr, len(inputs), C.byref(cp), kind, format, device,
+                                    str(path).encode() if path else None, C.byref(img),
+                                    C.byref(ln), err, len(err))
+    if rc:
+        _raise(rc, err)
+    try:
+        return _take_bytes(img, ln.value)
+    finally:
+        N.lib.cobs_gpu_free(img)
+
+
 def last_build_timing() -> Tuple[float, float, float]:
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     N.lib.cobs_gpu_build_timing(C.byref(a), C.byref(b), C.byref(c))

@@ -87,6 +87,11 @@ SIGNATURES = {
                                     C.c_uint32, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_uint64),
                                     C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_merge_classic": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    "cobs_gpu_query_fasta": (C.c_int, [vp, C.c_char_p, C.c_double, C.c_uint64, C.POINTER(vp),
+                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
+    "cobs_gpu_build_files": (C.c_int, [C.POINTER(C.c_char_p), C.c_uint64, C.POINTER(IndexParamsC),
+                                       C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp),
+                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
     "cobs_gpu_build_timing": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]),
     "cobs_gpu_free": (None, [vp]),

@@ -8,6 +8,7 @@
 
 #include "../../include/cobs_gpu.h"
 #include "build.hpp"
+#include "frontend.hpp"
 #include "index.hpp"
 #include "merge.hpp"
 
@@ -306,6 +307,39 @@ int cobs_gpu_merge_classic(const cobs_gpu_index* a, const cobs_gpu_index* b, int
         auto h = std::make_unique<cobs_gpu_index>();
         h->ix = cobsg::merge_classic(*a->ix, *b->ix, device);
         *out = h.release();
+    });
+}
+
+int cobs_gpu_query_fasta(cobs_gpu_index* index, const char* fasta_path, double K, uint64_t top_t,
+                         char** tsv, uint64_t* tsv_len, char* err, size_t errlen) {
+    *tsv = nullptr;
+    *tsv_len = 0;
+    return guarded(err, errlen, [&] {
+        std::string out = cobsg::query_fasta_tsv(*index->ix, fasta_path, K, top_t);
+        *tsv = static_cast<char*>(std::malloc(out.size() + 1));
+        if (!*tsv) throw std::bad_alloc();
+        std::memcpy(*tsv, out.c_str(), out.size() + 1);
+        *tsv_len = out.size();
+    });
+}
+
+int cobs_gpu_build_files(const char* const* inputs, uint64_t n_inputs, const cobs_index_params* params,
+                         int kind, int format, int device, const char* out_path, uint8_t** image,
+                         uint64_t* image_len, char* err, size_t errlen) {
+    if (image) *image = nullptr;
+    if (image_len) *image_len = 0;
+    return guarded(err, errlen, [&] {
+        if (format < COBS_FORMAT_AUTO || format > COBS_FORMAT_TEXT) throw cobsg::UsageError("unknown input format");
+        std::vector<std::string> in(inputs, inputs + n_inputs);
+        std::vector<uint8_t> img =
+            cobsg::build_from_files(in, to_params(params), static_cast<uint8_t>(kind), format, device);
+        if (out_path) cobsg::write_image(img, out_path);
+        if (image) {
+            *image = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
+            if (!*image) throw std::bad_alloc();
+            std::memcpy(*image, img.data(), img.size());
+            *image_len = img.size();
+        }
     });
 }
 
