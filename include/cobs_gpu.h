@@ -65,6 +65,20 @@ const char* cobs_gpu_version(void);
 int cobs_gpu_index_open(const char* path, int device, cobs_gpu_index** out, char* err,
                         size_t errlen);
 
+/* Same with an HBM budget (bytes).  If the pitched payload exceeds a
+ * non-zero budget the index opens in the host-resident streaming mode
+ * (the counterpart of open_random_access,
+ * storage.hpp:21-23): the payload stays in pinned host memory and each query
+ * batch streams it through two staging buffers of budget/2 bytes, copies
+ * overlapping the gather.  Results are identical to the resident mode. */
+int cobs_gpu_index_open_ex(const char* path, int device, uint64_t hbm_budget, cobs_gpu_index** out,
+                           char* err, size_t errlen);
+/* cobs_gpu_index_open_ex from an in-memory file image. */
+int cobs_gpu_index_open_image_ex(const uint8_t* image, uint64_t len, const char* path, int device,
+                                 uint64_t hbm_budget, cobs_gpu_index** out, char* err, size_t errlen);
+/* 1 if the index is in the host-resident streaming mode. */
+int cobs_gpu_index_streaming(const cobs_gpu_index* index);
+
 /* Same, from an in-memory file image (`path` is only used in messages). */
 int cobs_gpu_index_open_image(const uint8_t* image, uint64_t len, const char* path, int device,
                               cobs_gpu_index** out, char* err, size_t errlen);
@@ -154,6 +168,9 @@ uint32_t cobs_gpu_results_launches(const cobs_gpu_results* r);
 /* Algorithmic row bytes of the batch: sum_i k * l_i * sum_b row_bytes_b
  * (the random-access reader's bytes_read accounting, storage.cpp:325-331). */
 uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r);
+/* Streaming mode: index payload bytes copied host -> HBM by the batch (the
+ * analogue of RandomAccessView::bytes_read, index_view.hpp:44-46). */
+uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r);
 void cobs_gpu_results_free(cobs_gpu_results* r);
 
 /* ---- build ------------------------------------------------------------ */

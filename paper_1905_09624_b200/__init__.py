@@ -120,6 +120,7 @@ class BatchResult:
     ms_total: float
     launches: int
     row_bytes: int
+    h2d_index_bytes: int = 0
 
     def hits(self, i: int) -> Tuple[np.ndarray, np.ndarray]:
         o, n = int(self.hit_off[i]), int(self.hit_n[i])
@@ -179,6 +180,9 @@ class DeviceIndexView:
     def total_docs(self) -> int:
         return int(N.lib.cobs_gpu_index_total_docs(self._h))
 
+    def streaming(self) -> bool:
+        return bool(N.lib.cobs_gpu_index_streaming(self._h))
+
     def device_bytes(self) -> int:
         return int(N.lib.cobs_gpu_index_device_bytes(self._h))
 
@@ -217,13 +221,27 @@ def open_resident(path: str, device: int = 0) -> DeviceIndexView:
     return DeviceIndexView(h.value)
 
 
-def open_image(image: bytes, device: int = 0, path: str = "<memory>") -> DeviceIndexView:
-    """open_resident over an in-memory file image."""
+def open_random_access(path: str, hbm_budget: int, device: int = 0) -> DeviceIndexView:
+    """Host-resident streaming mode when the pitched payload exceeds
+    hbm_budget (the counterpart of cobs::open_random_access, storage.hpp:23)."""
+    h = C.c_void_p()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_index_open_ex(str(path).encode(), device, hbm_budget, C.byref(h), err,
+                                      len(err))
+    if rc:
+        _raise(rc, err)
+    return DeviceIndexView(h.value)
+
+
+def open_image(image: bytes, device: int = 0, path: str = "<memory>",
+               hbm_budget: int = 0) -> DeviceIndexView:
+    """open_resident over an in-memory file image (streaming mode when the
+    pitched payload exceeds a non-zero hbm_budget)."""
     h = C.c_void_p()
     err = _errbuf()
     buf = np.frombuffer(image, dtype=np.uint8)
-    rc = N.lib.cobs_gpu_index_open_image(buf.ctypes.data, len(image), path.encode(), device,
-                                         C.byref(h), err, len(err))
+    rc = N.lib.cobs_gpu_index_open_image_ex(buf.ctypes.data, len(image), path.encode(), device,
+                                            hbm_budget, C.byref(h), err, len(err))
     if rc:
         _raise(rc, err)
     return DeviceIndexView(h.value)
@@ -334,7 +352,8 @@ def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: 
             docs=arr(dd, total.value, np.uint32), scores=arr(ss, total.value, np.uint32),
             dense=dense, ms_termize=t[0].value, ms_gather=t[1].value, ms_order=t[2].value,
             ms_total=t[3].value, launches=int(N.lib.cobs_gpu_results_launches(r)),
-            row_bytes=int(N.lib.cobs_gpu_results_row_bytes(r)))
+            row_bytes=int(N.lib.cobs_gpu_results_row_bytes(r)),
+            h2d_index_bytes=int(N.lib.cobs_gpu_results_h2d_index_bytes(r)))
     finally:
         N.lib.cobs_gpu_results_free(r)
 

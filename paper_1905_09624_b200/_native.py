@@ -45,6 +45,11 @@ SIGNATURES = {
     "cobs_gpu_index_open": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_index_open_image": (C.c_int, [vp, C.c_uint64, C.c_char_p, C.c_int, C.POINTER(vp),
                                             C.c_char_p, C.c_size_t]),
+    "cobs_gpu_index_open_ex": (C.c_int, [C.c_char_p, C.c_int, C.c_uint64, C.POINTER(vp), C.c_char_p,
+                                         C.c_size_t]),
+    "cobs_gpu_index_open_image_ex": (C.c_int, [vp, C.c_uint64, C.c_char_p, C.c_int, C.c_uint64,
+                                               C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    "cobs_gpu_index_streaming": (C.c_int, [vp]),
     "cobs_gpu_index_close": (None, [vp]),
     "cobs_gpu_index_set_stream": (C.c_int, [vp, vp]),
     "cobs_gpu_index_params": (C.c_int, [vp, C.POINTER(IndexParamsC)]),
@@ -78,6 +83,7 @@ SIGNATURES = {
                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "cobs_gpu_results_launches": (C.c_uint32, [vp]),
     "cobs_gpu_results_row_bytes": (C.c_uint64, [vp]),
+    "cobs_gpu_results_h2d_index_bytes": (C.c_uint64, [vp]),
     "cobs_gpu_results_free": (None, [vp]),
     "cobs_gpu_build": (C.c_int, [vp, vp, C.c_uint64, vp, C.POINTER(C.c_char_p), C.c_uint64,
                                  C.POINTER(IndexParamsC), C.c_int, C.c_uint64, C.c_int, C.c_char_p,

@@ -396,6 +396,10 @@ std::vector<uint8_t> index_image(const DeviceIndex& ix) {
     const uint64_t payload = ix.meta.file_size - ix.meta.payload_start;
     std::vector<uint8_t> image(header.size() + payload);
     std::memcpy(image.data(), header.data(), header.size());
+    if (ix.streaming()) { // host-resident: the payload is already in file layout
+        std::memcpy(image.data() + header.size(), ix.hs->host, payload);
+        return image;
+    }
     COBS_CUDA(cudaSetDevice(ix.device));
     uint64_t off = header.size();
     for (const DevBlock& d : ix.blocks) { // un-pitch on the copy engine

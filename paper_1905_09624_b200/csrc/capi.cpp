@@ -66,6 +66,29 @@ extern "C" {
 
 const char* cobs_gpu_version(void) { return "cobs-b200 0.1 (sm_100a)"; }
 
+int cobs_gpu_index_open_ex(const char* path, int device, uint64_t hbm_budget, cobs_gpu_index** out,
+                           char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::open_index(cobsg::file_source(path), device, hbm_budget);
+        *out = h.release();
+    });
+}
+
+int cobs_gpu_index_open_image_ex(const uint8_t* image, uint64_t len, const char* path, int device,
+                                 uint64_t hbm_budget, cobs_gpu_index** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::open_index(cobsg::memory_source(image, len, path ? path : "<memory>"), device,
+                                  hbm_budget);
+        *out = h.release();
+    });
+}
+
+int cobs_gpu_index_streaming(const cobs_gpu_index* index) { return index->ix->streaming() ? 1 : 0; }
+
 int cobs_gpu_index_open(const char* path, int device, cobs_gpu_index** out, char* err, size_t errlen) {
     *out = nullptr;
     return guarded(err, errlen, [&] {
@@ -133,7 +156,10 @@ uint64_t cobs_gpu_index_doc_global(const cobs_gpu_index* index, uint64_t b, uint
     return index->ix->meta.blocks[b].doc_base + i;
 }
 
-uint64_t cobs_gpu_index_device_bytes(const cobs_gpu_index* index) { return index->ix->payload_bytes; }
+uint64_t cobs_gpu_index_device_bytes(const cobs_gpu_index* index) {
+    const cobsg::DeviceIndex& ix = *index->ix;
+    return ix.streaming() ? 2 * ix.hs->staging_bytes : ix.payload_bytes;
+}
 
 int cobs_gpu_index_row(const cobs_gpu_index* index, uint64_t b, uint64_t r, uint64_t lo, uint64_t hi,
                        uint8_t* out) {
@@ -141,6 +167,10 @@ int cobs_gpu_index_row(const cobs_gpu_index* index, uint64_t b, uint64_t r, uint
         const cobsg::DeviceIndex& ix = *index->ix;
         if (b >= ix.blocks.size() || r >= ix.blocks[b].w || lo > hi || hi > ix.blocks[b].rb)
             throw cobsg::UsageError("row: out of range");
+        if (ix.streaming()) {
+            std::memcpy(out, ix.hs->host + ix.hs->block_off[b] + r * ix.blocks[b].rb + lo, hi - lo);
+            return;
+        }
         COBS_CUDA(cudaSetDevice(ix.device));
         COBS_CUDA(cudaMemcpy(out, ix.payload + ix.blocks[b].base + r * ix.blocks[b].pitch + lo, hi - lo,
                              cudaMemcpyDeviceToHost));
@@ -157,6 +187,11 @@ int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* er
         std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
         if (std::fwrite(head.data(), 1, head.size(), f) != head.size())
             throw cobsg::DataError(std::string("error writing index file: ") + path);
+        if (ix.streaming()) {
+            if (std::fwrite(ix.hs->host, 1, ix.hs->host_bytes, f) != ix.hs->host_bytes)
+                throw cobsg::DataError(std::string("error writing index file: ") + path);
+            return;
+        }
         std::vector<uint8_t> buf;
         for (const cobsg::DevBlock& d : ix.blocks) {
             uint64_t rows_per = std::max<uint64_t>(1, (64ull << 20) / d.rb);
@@ -256,6 +291,8 @@ int cobs_gpu_results_timing(const cobs_gpu_results* r, double* a, double* b, dou
 uint32_t cobs_gpu_results_launches(const cobs_gpu_results* r) { return r->r.launches; }
 
 uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r) { return r->r.row_bytes; }
+
+uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r) { return r->r.h2d_index_bytes; }
 
 void cobs_gpu_results_free(cobs_gpu_results* r) { delete r; }
 

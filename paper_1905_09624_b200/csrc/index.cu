@@ -43,9 +43,22 @@ DeviceIndex::~DeviceIndex() {
     if (stream) cudaStreamDestroy(stream);
 }
 
-void DeviceIndex::allocate() {
+HostStream::~HostStream() {
+    if (copy) cudaStreamSynchronize(copy);
+    for (int i = 0; i < 2; ++i) {
+        if (staging[i]) cudaFree(staging[i]);
+        if (copied[i]) cudaEventDestroy(copied[i]);
+        if (consumed[i]) cudaEventDestroy(consumed[i]);
+    }
+    if (d_slab_blocks) cudaFree(d_slab_blocks);
+    if (d_slab_ct) cudaFree(d_slab_ct);
+    if (host) cudaFreeHost(host);
+    if (copy) cudaStreamDestroy(copy);
+}
+
+void DeviceIndex::plan() {
     COBS_CUDA(cudaSetDevice(device));
-    COBS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    if (!stream) COBS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     if (meta.total_docs() >= (1ull << 32))
         throw DataError("index has more than 2^32 documents; the device path indexes columns in 32 bits");
     uint64_t off = 0;
@@ -53,7 +66,6 @@ void DeviceIndex::allocate() {
     blocks.clear();
     ct_block.clear();
     ct_slice.clear();
-    bool any_pad = false;
     for (size_t b = 0; b < meta.blocks.size(); ++b) {
         const BlockMeta& m = meta.blocks[b];
         DevBlock d{};
@@ -67,7 +79,6 @@ void DeviceIndex::allocate() {
         uint64_t bytes = m.w * d.pitch;
         if (m.w != 0 && bytes / m.w != d.pitch) throw DataError("block payload too large for the device");
         off += (bytes + 255) & ~255ull;
-        any_pad |= d.pitch != d.rb;
         sum_row_bytes += d.rb;
         blocks.push_back(d);
         uint32_t slices = (d.rb + 127u) / 128u;
@@ -77,6 +88,15 @@ void DeviceIndex::allocate() {
         }
     }
     payload_bytes = off;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    evict_first = payload_bytes > 4ull * static_cast<uint64_t>(l2);
+}
+
+void DeviceIndex::allocate() {
+    plan();
+    bool any_pad = false;
+    for (const DevBlock& d : blocks) any_pad |= d.pitch != d.rb;
     size_t free_b = 0, total_b = 0;
     COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     if (payload_bytes + (256ull << 20) > free_b)
@@ -89,9 +109,6 @@ void DeviceIndex::allocate() {
             if (d.pitch != d.rb)
                 COBS_CUDA(cudaMemsetAsync(payload + d.base, 0, d.w * d.pitch, stream));
     }
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
-    evict_first = payload_bytes > 4ull * static_cast<uint64_t>(l2);
 }
 
 void DeviceIndex::finish_upload() {
@@ -113,10 +130,97 @@ void DeviceIndex::finish_upload() {
     COBS_CUDA(cudaStreamSynchronize(stream));
 }
 
-std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device) {
+namespace {
+
+// Host-resident mode: read the payload into pinned memory, cut blocks into
+// slabs of whole 1,024-document slices that fit half the budget, pack slabs
+// into groups (one staging buffer each), upload the slab tables.
+void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
+    auto hs = std::make_unique<HostStream>();
+    const IndexMeta& m = ix.meta;
+    hs->host_bytes = m.file_size - m.payload_start;
+    COBS_CUDA(cudaHostAlloc(&hs->host, std::max<uint64_t>(hs->host_bytes, 1), cudaHostAllocDefault));
+    for (uint64_t o = 0; o < hs->host_bytes; o += (1ull << 30)) {
+        uint64_t len = std::min<uint64_t>(1ull << 30, hs->host_bytes - o);
+        src.read_at(m.payload_start + o, hs->host + o, len);
+    }
+    const uint64_t half = (budget / 2) & ~255ull;
+    hs->staging_bytes = half;
+    std::vector<DevBlock> sblocks;
+    std::vector<uint32_t> sct;
+    StreamGroup g{0, 0, 0, 0};
+    uint64_t used = 0;
+    for (size_t b = 0; b < ix.blocks.size(); ++b) {
+        const DevBlock& d = ix.blocks[b];
+        hs->block_off.push_back(m.blocks[b].offset - m.payload_start);
+        const uint32_t nsl = (d.rb + 127u) / 128u;
+        const uint64_t per_slice = d.w * 128ull;
+        uint32_t s_max = static_cast<uint32_t>(std::max<uint64_t>(1, half / std::max<uint64_t>(per_slice, 1)));
+        for (uint32_t s0 = 0; s0 < nsl; s0 += s_max) {
+            Slab sl{};
+            sl.block = static_cast<uint32_t>(b);
+            sl.s0 = s0;
+            sl.ns = std::min(s_max, nsl - s0);
+            sl.width = std::min<uint32_t>(d.rb - s0 * 128u, sl.ns * 128u);
+            sl.pitch = (sl.width + 31u) & ~31u;
+            const uint64_t bytes = ((d.w * sl.pitch) + 255) & ~255ull;
+            if (bytes > half)
+                throw DataError("block " + std::to_string(b) + " needs " + std::to_string(bytes) +
+                                " bytes of HBM per slice, more than half the budget");
+            if (used + bytes > half) { // close the group
+                g.slab_hi = static_cast<uint32_t>(hs->slabs.size());
+                g.ct_hi = static_cast<uint32_t>(sct.size() / 2);
+                hs->groups.push_back(g);
+                g = StreamGroup{g.slab_hi, 0, g.ct_hi, 0};
+                used = 0;
+            }
+            sl.base = used;
+            used += bytes;
+            DevBlock sd = d;
+            sd.base = sl.base;
+            sd.pitch = sl.pitch;
+            sd.rb = sl.width;
+            sd.dc = std::min<uint32_t>(d.dc - s0 * 1024u, sl.ns * 1024u);
+            sd.doc_base = d.doc_base + s0 * 1024u;
+            const uint32_t idx = static_cast<uint32_t>(hs->slabs.size());
+            for (uint32_t j = 0; j < sl.ns; ++j) {
+                sct.push_back(idx);
+                sct.push_back(j);
+            }
+            hs->slabs.push_back(sl);
+            sblocks.push_back(sd);
+        }
+    }
+    g.slab_hi = static_cast<uint32_t>(hs->slabs.size());
+    g.ct_hi = static_cast<uint32_t>(sct.size() / 2);
+    if (g.slab_hi > g.slab_lo) hs->groups.push_back(g);
+    COBS_CUDA(cudaMalloc(&hs->d_slab_blocks, sizeof(DevBlock) * std::max<size_t>(sblocks.size(), 1)));
+    COBS_CUDA(cudaMalloc(&hs->d_slab_ct, sizeof(uint32_t) * std::max<size_t>(sct.size(), 2)));
+    COBS_CUDA(cudaMemcpy(hs->d_slab_blocks, sblocks.data(), sizeof(DevBlock) * sblocks.size(),
+                         cudaMemcpyHostToDevice));
+    COBS_CUDA(cudaMemcpy(hs->d_slab_ct, sct.data(), sizeof(uint32_t) * sct.size(), cudaMemcpyHostToDevice));
+    for (int i = 0; i < 2; ++i) {
+        COBS_CUDA(cudaMalloc(&hs->staging[i], std::max<uint64_t>(half, 256)));
+        COBS_CUDA(cudaEventCreateWithFlags(&hs->copied[i], cudaEventDisableTiming));
+        COBS_CUDA(cudaEventCreateWithFlags(&hs->consumed[i], cudaEventDisableTiming));
+    }
+    COBS_CUDA(cudaStreamCreateWithFlags(&hs->copy, cudaStreamNonBlocking));
+    ix.evict_first = true;
+    ix.hs = std::move(hs);
+}
+
+} // namespace
+
+std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget) {
     auto ix = std::make_unique<DeviceIndex>();
     ix->meta = parse_index(src);
     ix->device = device;
+    ix->plan();
+    if (hbm_budget > 0 && ix->payload_bytes > hbm_budget) {
+        open_streaming(*ix, src, hbm_budget);
+        ix->finish_upload();
+        return ix;
+    }
     ix->allocate();
     // Stream rows through two pinned staging buffers, re-pitching on the copy
     // engine (cudaMemcpy2DAsync), while the next chunk is read from the file.

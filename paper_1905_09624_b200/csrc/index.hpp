@@ -40,6 +40,35 @@ struct QueryWorkspace {
     uint64_t hit_cap = 0;
 };
 
+// Host-resident (out-of-core) mode: the payload stays in
+// pinned host memory in file layout and every query batch streams it through
+// two HBM staging buffers in "slabs" (a block's rows restricted to a range of
+// 1,024-document slices), copy of slab group g+1 overlapping the gather of
+// group g.  The counterpart of the reference's random-access reader
+// (storage.cpp:320-341) for indexes larger than HBM.
+struct Slab {
+    uint32_t block, s0, ns; // slices [s0, s0+ns) of `block`
+    uint64_t base;          // offset inside the staging buffer
+    uint32_t width, pitch;  // row bytes copied / device row stride
+};
+struct StreamGroup {
+    uint32_t slab_lo, slab_hi, ct_lo, ct_hi;
+};
+struct HostStream {
+    uint8_t* host = nullptr;         // pinned; the file's payload bytes
+    uint64_t host_bytes = 0;
+    std::vector<uint64_t> block_off; // payload offset of each block
+    std::vector<Slab> slabs;
+    std::vector<StreamGroup> groups;
+    DevBlock* d_slab_blocks = nullptr;
+    uint32_t* d_slab_ct = nullptr;   // (slab, local slice) pairs, group by group
+    uint8_t* staging[2] = {nullptr, nullptr};
+    uint64_t staging_bytes = 0;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    ~HostStream();
+};
+
 struct DeviceIndex {
     IndexMeta meta;
     int device = 0;
@@ -58,15 +87,21 @@ struct DeviceIndex {
     bool evict_first = false;   // payload far larger than L2
     std::mutex mu;
     QueryWorkspace ws;
+    std::unique_ptr<HostStream> hs; // non-null: host-resident (streaming) mode
+    bool streaming() const { return hs != nullptr; }
 
     ~DeviceIndex();
-    // Set up blocks / tasks / ranks from `meta` and allocate the payload.
+    // Block table, column tasks and pitched layout from `meta` (no memory).
+    void plan();
+    // plan() + allocate the pitched payload in HBM.
     void allocate();
     void finish_upload(); // block table, tasks, ranks -> HBM
 };
 
 // Open from a byte source: parse, allocate, stream rows into pitched HBM.
-std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device);
+// With hbm_budget > 0 and a pitched payload larger than it, open in the
+// host-resident streaming mode with two staging buffers of hbm_budget/2.
+std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget = 0);
 // Config-5 procedural index generated in HBM.
 std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n_docs, uint64_t block_size,
                                             double median, double sigma, double p, int device);
@@ -83,6 +118,7 @@ struct QueryResults {
     uint32_t score_bytes = 2;
     double ms_termize = 0, ms_gather = 0, ms_order = 0, ms_total = 0;
     uint32_t launches = 0; // kernels of ours launched by the batch
+    uint64_t h2d_index_bytes = 0; // streaming mode: payload bytes copied to HBM
     uint64_t row_bytes = 0;
 };
 

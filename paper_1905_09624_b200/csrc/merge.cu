@@ -48,6 +48,8 @@ __global__ void concat_kernel(const uint8_t* a, uint32_t pa, uint32_t ra, uint64
 std::unique_ptr<DeviceIndex> merge_classic(const DeviceIndex& A, const DeviceIndex& B, int device) {
     const IndexMeta& a = A.meta;
     const IndexMeta& b = B.meta;
+    if (A.streaming() || B.streaming())
+        throw UsageError("merge: host-resident (streaming) indexes are not supported");
     if (a.kind != kKindClassic || b.kind != kKindClassic)
         throw UsageError("merge: only classic indexes can be merged");
     const Params &pa = a.params, &pb = b.params; // IndexParams::operator== (params.hpp:37)

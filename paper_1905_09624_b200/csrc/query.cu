@@ -747,9 +747,40 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
         COBS_CUDA(cudaMemsetAsync(ws.hit_count.ptr, 0, 4 * n, st));
         COBS_CUDA(cudaMemsetAsync(ws.hit_total.ptr, 0, 8, st));
         if (attempt == 0) COBS_CUDA(cudaEventRecord(ev[1], st));
-        if (grid2 > 0) {
-            fn<<<static_cast<unsigned>(grid2), 256, 0, st>>>(ga);
-            R.launches += 1;
+        if (!ix.streaming()) {
+            if (grid2 > 0) {
+                fn<<<static_cast<unsigned>(grid2), 256, 0, st>>>(ga);
+                R.launches += 1;
+            }
+        } else { // host-resident index: stream slab groups through two staging buffers
+            HostStream& hs = *ix.hs;
+            for (size_t gi = 0; gi < hs.groups.size(); ++gi) {
+                const StreamGroup& G = hs.groups[gi];
+                const int buf = static_cast<int>(gi & 1);
+                COBS_CUDA(cudaStreamWaitEvent(hs.copy, hs.consumed[buf], 0)); // buffer free again
+                for (uint32_t si = G.slab_lo; si < G.slab_hi; ++si) {
+                    const Slab& sl = hs.slabs[si];
+                    const DevBlock& d = ix.blocks[sl.block];
+                    COBS_CUDA(cudaMemcpy2DAsync(hs.staging[buf] + sl.base, sl.pitch,
+                                                hs.host + hs.block_off[sl.block] + sl.s0 * 128ull, d.rb,
+                                                sl.width, d.w, cudaMemcpyHostToDevice, hs.copy));
+                    R.h2d_index_bytes += d.w * sl.width;
+                }
+                COBS_CUDA(cudaEventRecord(hs.copied[buf], hs.copy));
+                COBS_CUDA(cudaStreamWaitEvent(st, hs.copied[buf], 0));
+                GatherArgs gg = ga;
+                gg.payload = hs.staging[buf];
+                gg.blocks = hs.d_slab_blocks;
+                gg.ct = hs.d_slab_ct + 2ull * G.ct_lo;
+                gg.nct = G.ct_hi - G.ct_lo;
+                const uint64_t grid_g = tiles * ((qt + 7) / 8) * gg.nct;
+                if (grid_g >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
+                if (grid_g > 0) {
+                    fn<<<static_cast<unsigned>(grid_g), 256, 0, st>>>(gg);
+                    R.launches += 1;
+                }
+                COBS_CUDA(cudaEventRecord(hs.consumed[buf], st));
+            }
         }
         COBS_CUDA(cudaGetLastError());
         COBS_CUDA(cudaEventRecord(ev[2], st));

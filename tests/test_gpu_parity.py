@@ -282,3 +282,59 @@ def _packed(docs):
     np.cumsum([len(d[1]) for d in docs], out=doc_segs[1:])
     buf = np.frombuffer(b"".join(segs), np.uint8) if segs else np.zeros(1, np.uint8)
     return buf, off, doc_segs, names
+
+
+@pytest.mark.parametrize("kind,frac", [(0, 0.9), (1, 1.05), (1, 1.5)])
+def test_host_resident_streaming(gpu, tmp_path, kind, frac):
+    """Out-of-core mode: with an HBM budget below the pitched payload the index
+    stays in pinned host memory and batches stream it through two staging
+    buffers (slabs of a block's slices, several blocks per group); results are
+    identical to the resident index and the oracle; every batch copies the
+    whole payload once."""
+    from paper_1905_09624_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c2"], 3000 if kind == 0 else 2600, len_scale=0.001,
+                       n_queries=60, kind=kind, block_size=256, k=2)
+    docs = [(n, [s]) for n, s in zip(synth.doc_names(cfg), _doc_bytes(cfg))]
+    params = cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p, block_size=cfg.block_size)
+    img = cb.build_image(docs, params, kind, device=gpu)
+    path = str(tmp_path / "i.cobs")
+    open(path, "wb").write(img)
+    res = cb.open_resident(path, gpu)
+    pitched = res.device_bytes()
+    # classic: a fraction of the payload (slabs split the block's slices);
+    # compact: multiples of twice the largest block (several blocks per group)
+    biggest = max(res.width(i) * ((res.row_bytes(i) + 31) // 32 * 32) for i in range(res.block_count()))
+    budget = int(pitched * frac) if kind == 0 else int(2 * biggest * frac) + 4096
+    budget = min(budget, pitched - 256)
+    st = cb.open_random_access(path, budget, gpu)
+    assert st.streaming() and not res.streaming()
+    qb, qo = synth.queries(cfg)
+    a = cb.query_batch_raw(res, qb, qo, 1e-12, scores=True)
+    b = cb.query_batch_raw(st, qb, qo, 1e-12, scores=True)
+    assert np.array_equal(a.dense, b.dense)
+    assert np.array_equal(a.ell, b.ell)
+    payload = sum(st.width(i) * st.row_bytes(i) for i in range(st.block_count()))
+    assert b.h2d_index_bytes == payload and a.h2d_index_bytes == 0
+    for K, top_t in [(0.7, 0), (0.5, 4)]:
+        x = cb.query_batch_raw(res, qb, qo, K, top_t)
+        y = cb.query_batch_raw(st, qb, qo, K, top_t)
+        for i in range(len(qo) - 1):
+            assert gpu_hits(res, x, i) == gpu_hits(st, y, i)
+    idx = O.OracleIndex.parse(img)
+    ell, sk, s_, nh, dense = idx.query_batch(qb, qo, 1e-12, scores=True)
+    assert np.array_equal(b.dense.astype(np.uint32), dense)
+    assert cb.index_image(st) == img and st.row_data(0, 3) == res.row_data(0, 3)
+    res.close()
+    st.close()
+
+
+def _doc_bytes(cfg):
+    from paper_1905_09624_b200 import synth
+    buf, off = synth.docs(cfg)
+    return [buf[int(off[i]):int(off[i + 1])].tobytes() for i in range(cfg.n_docs)]
+
+
+def test_streaming_budget_too_small(gpu, tmp_path):
+    path = os.path.join(GDIR, "classic_k2.cobs")
+    with pytest.raises(cb.DataError, match="more than half the budget"):
+        cb.open_random_access(path, 1024, gpu)
