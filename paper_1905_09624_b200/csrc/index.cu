@@ -162,7 +162,10 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
             sl.s0 = s0;
             sl.ns = std::min(s_max, nsl - s0);
             sl.width = std::min<uint32_t>(d.rb - s0 * 128u, sl.ns * 128u);
-            sl.pitch = (sl.width + 31u) & ~31u;
+            // whole 4-byte-aligned rows go over as one contiguous copy at the
+            // file's own row length (narrow 2D DMA rows crawl over PCIe)
+            sl.direct = s0 == 0 && sl.width == d.rb && (d.rb & 3u) == 0;
+            sl.pitch = sl.direct ? sl.width : ((sl.width + 31u) & ~31u);
             const uint64_t bytes = ((d.w * sl.pitch) + 255) & ~255ull;
             if (bytes > half)
                 throw DataError("block " + std::to_string(b) + " needs " + std::to_string(bytes) +

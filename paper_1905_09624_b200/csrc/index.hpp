@@ -50,6 +50,7 @@ struct Slab {
     uint32_t block, s0, ns; // slices [s0, s0+ns) of `block`
     uint64_t base;          // offset inside the staging buffer
     uint32_t width, pitch;  // row bytes copied / device row stride
+    bool direct;            // whole rows, pitch == file row bytes: one 1D copy
 };
 struct StreamGroup {
     uint32_t slab_lo, slab_hi, ct_lo, ct_hi;

@@ -761,9 +761,13 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
                 for (uint32_t si = G.slab_lo; si < G.slab_hi; ++si) {
                     const Slab& sl = hs.slabs[si];
                     const DevBlock& d = ix.blocks[sl.block];
-                    COBS_CUDA(cudaMemcpy2DAsync(hs.staging[buf] + sl.base, sl.pitch,
-                                                hs.host + hs.block_off[sl.block] + sl.s0 * 128ull, d.rb,
-                                                sl.width, d.w, cudaMemcpyHostToDevice, hs.copy));
+                    if (sl.direct)
+                        COBS_CUDA(cudaMemcpyAsync(hs.staging[buf] + sl.base, hs.host + hs.block_off[sl.block],
+                                                  d.w * d.rb, cudaMemcpyHostToDevice, hs.copy));
+                    else
+                        COBS_CUDA(cudaMemcpy2DAsync(hs.staging[buf] + sl.base, sl.pitch,
+                                                    hs.host + hs.block_off[sl.block] + sl.s0 * 128ull, d.rb,
+                                                    sl.width, d.w, cudaMemcpyHostToDevice, hs.copy));
                     R.h2d_index_bytes += d.w * sl.width;
                 }
                 COBS_CUDA(cudaEventRecord(hs.copied[buf], hs.copy));
