@@ -1,0 +1,86 @@
+"""Edge cases on the GPU against the oracle: empty batches, zero-window and
+all-skipped patterns mixed with good ones, q = 1 / q > 32 / k = 5 (runtime-k
+path), raw non-ASCII bytes, exact-integer thresholds, top_t beyond the hits."""
+import random
+
+import numpy as np
+import pytest
+
+import paper_1905_09624_b200 as cb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rb(rng, n, alphabet):
+    return bytes(rng.choice(alphabet) for _ in range(n))
+
+
+def check(img, pats, Ks=(1e-12, 0.5, 1.0), tops=(0, 2, 10**9)):
+    view = cb.open_image(img, 0)
+    idx = O.OracleIndex.parse(img)
+    for K in Ks:
+        for top in tops:
+            b = cb.query_batch(view, pats, K, top, scores=True)
+            for i, p in enumerate(pats):
+                try:
+                    ell, sk, hits, dense = idx.query(p, K, top, scores=True)
+                except O.OracleError as e:
+                    assert (int(b.status[i]), b.messages[i]) == (e.code, e.msg)
+                    continue
+                assert (int(b.ell[i]), int(b.skipped[i])) == (ell, sk)
+                d, s = b.hits(i)
+                assert [(int(x), int(y)) for x, y in zip(d, s)] == hits
+                assert np.array_equal(b.dense[i].astype(np.uint32), dense)
+    view.close()
+
+
+def test_empty_batch(gpu):
+    img = O.build_image([(b"a", [b"ACGT" * 20])])
+    view = cb.open_image(img, 0)
+    b = cb.query_batch(view, [], 0.5)
+    assert len(b.ell) == 0 and len(b.docs) == 0
+    view.close()
+
+
+def test_mixed_error_and_good_patterns(gpu):
+    rng = random.Random(1)
+    docs = [(b"d%02d" % i, [rb(rng, 400, b"ACGT")]) for i in range(20)]
+    for canonical in (False, True):
+        img = O.build_image(docs, canonical=canonical, k=2)
+        pats = [b"", b"ACGT", docs[3][1][0][:80], b"N" * 31, b"N" * 100 + docs[4][1][0][:60],
+                docs[5][1][0][10:41], b"acgt" * 20, docs[6][1][0]]
+        check(img, pats)
+
+
+@pytest.mark.parametrize("q,k,alphabet,canonical", [
+    (1, 1, b"ACGT", False), (2, 3, b"ACGTN", True), (31, 5, b"ACGT", False),
+    (32, 2, b"ACGT", True), (40, 1, b"ACGT", True), (64, 2, b"ACGTN", False),
+    (7, 2, bytes(range(256)), False), (12, 1, b"\x00\xffAC", False)])
+def test_parameter_corners(gpu, q, k, alphabet, canonical):
+    rng = random.Random(q * 100 + k)
+    docs = [(b"doc%03d" % i, [rb(rng, rng.randint(0, 700), alphabet)]) for i in range(30)]
+    img = O.build_image(docs, q=q, k=k, canonical=canonical, block_size=7, kind=1)
+    assert cb.build_image(docs, cb.IndexParams(q=q, k=k, canonical=canonical, block_size=7), 1,
+                          device=0) == img
+    pats = []
+    for i in range(24):
+        src = docs[i][1][0]
+        if i % 3 == 0 or len(src) < q:
+            pats.append(rb(rng, rng.randint(0, 300), alphabet))
+        else:
+            st = rng.randrange(len(src) - q + 1)
+            pats.append(src[st:st + rng.randint(q, 300)])
+    check(img, pats)
+
+
+def test_exact_integer_thresholds(gpu):
+    """K * l an exact integer: tau must not be pushed up (bloom.cpp:120-123,
+    test_bloom.cpp:256-265)."""
+    rng = random.Random(9)
+    base = rb(rng, 2000, b"ACGT")
+    docs = [(b"x%d" % i, [base[: 100 * (i + 1)]]) for i in range(20)]
+    img = O.build_image(docs)
+    # patterns with l = 10, 20, 30, 100, 1000 distinct 31-mers
+    pats = [base[:31 + ell - 1] for ell in (10, 20, 30, 100, 1000)]
+    check(img, pats, Ks=(0.9, 0.1, 0.3, 0.7, 1.0), tops=(0,))
