@@ -17,6 +17,7 @@
 //               filled, not just the distinct ones.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <numeric>
@@ -46,9 +47,8 @@ struct WinArgs {
     int canonical;
 };
 
-// run g -> segment (seg_rbase[s] <= g < seg_rbase[s+1])
-__device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
-    uint64_t lo = a.seg_lo, hi = a.seg_hi;
+// run g -> segment (seg_rbase[s] <= g < seg_rbase[s+1]), searched in [lo, hi)
+__device__ __forceinline__ uint64_t find_seg_in(const WinArgs& a, uint64_t g, uint64_t lo, uint64_t hi) {
     while (hi - lo > 1) {
         uint64_t mid = (lo + hi) >> 1;
         if (a.seg_rbase[mid] <= g)
@@ -58,6 +58,14 @@ __device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
     }
     return lo;
 }
+__device__ __forceinline__ uint64_t find_seg(const WinArgs& a, uint64_t g) {
+    return find_seg_in(a, g, a.seg_lo, a.seg_hi);
+}
+
+// Runs are handed to CTAs in contiguous chunks so the segment range of a
+// chunk is searched once (by one thread) and each run's search is over the
+// few segments the chunk spans, not the whole corpus.
+constexpr uint64_t kChunkRuns = 512;
 
 // Calls f(j, dna, code) for the windows [j0, j1) of segment bytes `sb`
 // (dna: all-ACGT window with q <= 32, code: its canonical/forward code).
@@ -83,13 +91,22 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
                                                     unsigned long long* term_count) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t q = QC ? QC : a.q;
-    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t base = a.r_lo + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32;
-         base < a.r_hi; base += warps * 32) {
+    __shared__ uint64_t s_seg[2];
+    const uint64_t nchunks = (a.r_hi - a.r_lo + kChunkRuns - 1) / kChunkRuns;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t r0 = a.r_lo + c * kChunkRuns, r1 = min(a.r_hi, r0 + kChunkRuns);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_seg[0] = find_seg(a, r0);
+        s_seg[1] = find_seg(a, r1 - 1) + 1;
+    }
+    __syncthreads();
+    const uint64_t slo = s_seg[0], shi = s_seg[1];
+    for (uint64_t base = r0 + (threadIdx.x >> 5) * 32; base < r1; base += blockDim.x) {
         const uint64_t g = base + lane;
         uint32_t cnt = 0, doc = 0xffffffffu;
-        if (g < a.r_hi) {
-            const uint64_t s = find_seg(a, g);
+        if (g < r1) {
+            const uint64_t s = find_seg_in(a, g, slo, shi);
             doc = a.seg_doc[s];
             const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
             const uint64_t W = len >= q ? len - q + 1 : 0;
@@ -118,8 +135,9 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
         // one atomic per (warp, document)
         const unsigned peers = __match_any_sync(0xffffffffu, doc);
         const uint32_t sum = __reduce_add_sync(peers, cnt);
-        if (g < a.r_hi && sum && lane == (uint32_t)(__ffs(peers) - 1))
+        if (g < r1 && sum && lane == (uint32_t)(__ffs(peers) - 1))
             atomicAdd(term_count + doc, (unsigned long long)sum);
+    }
     }
 }
 
@@ -133,9 +151,19 @@ __global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* b
                                                    const uint32_t* doc_block, const uint32_t* doc_col,
                                                    unsigned int* words) {
     const uint32_t q = QC ? QC : a.q;
-    for (uint64_t g = a.r_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < a.r_hi;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = find_seg(a, g);
+    __shared__ uint64_t s_seg[2];
+    const uint64_t nchunks = (a.r_hi - a.r_lo + kChunkRuns - 1) / kChunkRuns;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t r0 = a.r_lo + c * kChunkRuns, r1 = min(a.r_hi, r0 + kChunkRuns);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_seg[0] = find_seg(a, r0);
+        s_seg[1] = find_seg(a, r1 - 1) + 1;
+    }
+    __syncthreads();
+    const uint64_t slo = s_seg[0], shi = s_seg[1];
+    for (uint64_t g = r0 + threadIdx.x; g < r1; g += blockDim.x) {
+        const uint64_t s = find_seg_in(a, g, slo, shi);
         const uint32_t doc = a.seg_doc[s];
         const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
         const uint64_t W = len >= q ? len - q + 1 : 0;
@@ -161,6 +189,7 @@ __global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* b
                 for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_term(w, q, false, seed));
             }
         });
+    }
     }
 }
 
@@ -266,46 +295,56 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     COBS_CUDA(cudaEventCreate(&e2));
     COBS_CUDA(cudaEventCreate(&e3));
 
-    // ---- count pass, in document chunks bounded by set memory ----------
+    // ---- count pass, in waves of documents whose sets fit in L2 ---------
+    // (random CAS into L2-resident sets instead of DRAM; a document larger
+    // than a wave gets a wave of its own)
     std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
     for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] + doc_w[d] / 2 + 1);
     size_t free_b = 0, total_b = 0;
     COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t budget_slots = std::max<uint64_t>((free_b / 3) / 8, 1ull << 20);
-    d_taboff.reserve(8 * n_docs);
-    d_tabslots.reserve(8 * n_docs);
-    COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
-    float ms_count = 0;
+    uint64_t wave_bytes = 96ull << 20;
+    if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
+    const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
+    std::vector<uint64_t> wave_lo{0};
+    uint64_t max_slots = 0;
     for (uint64_t d0 = 0; d0 < n_docs;) {
         uint64_t d1 = d0, slots = 0;
         while (d1 < n_docs && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
-            tab_off[d1] = slots;
+            tab_off[d1] = slots; // relative to the wave's tables
             slots += tab_slots[d1];
             ++d1;
         }
-        d_tab.reserve(8 * slots);
-        COBS_CUDA(cudaMemcpyAsync(d_taboff.as<uint64_t>() + d0, tab_off.data() + d0, 8 * (d1 - d0),
-                                  cudaMemcpyHostToDevice, st));
-        COBS_CUDA(cudaEventRecord(e0, st));
+        max_slots = std::max(max_slots, slots);
+        wave_lo.push_back(d1);
+        d0 = d1;
+    }
+    d_taboff.reserve(8 * n_docs);
+    d_tabslots.reserve(8 * n_docs);
+    d_tab.reserve(8 * max_slots);
+    COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaMemcpyAsync(d_taboff.ptr, tab_off.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+    COBS_CUDA(cudaEventRecord(e0, st));
+    auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
+    for (size_t wv = 0; wv + 1 < wave_lo.size(); ++wv) {
+        const uint64_t d0 = wave_lo[wv], d1 = wave_lo[wv + 1];
+        const uint64_t slots = tab_off[d1 - 1] + tab_slots[d1 - 1];
         COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
         wa.seg_lo = doc_segs[d0];
         wa.seg_hi = doc_segs[d1];
         wa.r_lo = seg_rbase[wa.seg_lo];
         wa.r_hi = seg_rbase[wa.seg_hi];
         if (wa.r_hi > wa.r_lo) {
-            // tab_off of the chunk's documents is relative to the chunk's tables
-            auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
-            ck<<<148 * 8, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
-                                        d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
+            const uint64_t runs = wa.r_hi - wa.r_lo;
+            const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (runs + kChunkRuns - 1) / kChunkRuns));
+            ck<<<grid, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
+                                     d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
             COBS_CUDA(cudaGetLastError());
         }
-        COBS_CUDA(cudaEventRecord(e1, st));
-        COBS_CUDA(cudaStreamSynchronize(st));
-        float t = 0;
-        cudaEventElapsedTime(&t, e0, e1);
-        ms_count += t;
-        d0 = d1;
     }
+    COBS_CUDA(cudaEventRecord(e1, st));
+    COBS_CUDA(cudaStreamSynchronize(st));
+    float ms_count = 0;
+    cudaEventElapsedTime(&ms_count, e0, e1);
     g_timing.ms_count = ms_count;
     std::vector<uint64_t> tc(n_docs);
     COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
