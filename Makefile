@@ -10,7 +10,7 @@ OBJS := $(OUT)/host.o $(OUT)/frontend.o $(OUT)/index.o $(OUT)/query.o $(OUT)/bui
         $(OUT)/capi.o
 HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh $(SRC)/*.h) include/cobs_gpu.h
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle cpptest clean
 all: lib oracle
 lib: $(OUT)/libcobs_gpu.so $(OUT)/libcobs_synth.so
 
@@ -39,6 +39,19 @@ $(OUT)/libcobs_gpu.so: $(OBJS)
 
 oracle:
 	$(MAKE) -C oracle
+
+# C++ host-API parity tests (tests/cpp): need the library and the oracle
+cpptest: tests/cpp/test_cobs_b200
+
+tests/cpp/test_cobs_b200: tests/cpp/test_cobs_b200.cpp include/cobs_b200.hpp include/cobs_gpu.h \
+		$(OUT)/libcobs_gpu.so oracle/_build/libcobs_oracle.so
+	g++ -std=c++20 -O2 -Wall -Iinclude -Ioracle -o $@ $< \
+	    -L$(OUT) -lcobs_gpu -Loracle/_build -lcobs_oracle \
+	    -Wl,-rpath,$(abspath $(OUT)) -Wl,-rpath,$(abspath oracle/_build) \
+	    -Wl,-rpath,'$$ORIGIN/../../$(OUT)' -Wl,-rpath,'$$ORIGIN/../../oracle/_build'
+
+oracle/_build/libcobs_oracle.so:
+	$(MAKE) -C oracle oracle
 
 clean:
 	rm -rf $(OUT) oracle/_build
