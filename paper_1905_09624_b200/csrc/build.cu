@@ -289,11 +289,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     wa.k = P.k;
     wa.canonical = P.canonical ? 1 : 0;
 
-    cudaEvent_t e0, e1, e2, e3;
-    COBS_CUDA(cudaEventCreate(&e0));
-    COBS_CUDA(cudaEventCreate(&e1));
-    COBS_CUDA(cudaEventCreate(&e2));
-    COBS_CUDA(cudaEventCreate(&e3));
+    Event e0, e1, e2, e3;
 
     // ---- count pass, in waves of documents whose sets fit in L2 ---------
     // (random CAS into L2-resident sets instead of DRAM; a document larger
@@ -421,10 +417,6 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     float ms_fill = 0;
     cudaEventElapsedTime(&ms_fill, e2, e3);
     g_timing.ms_fill = ms_fill;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    cudaEventDestroy(e3);
     ix->finish_upload();
     g_timing.ms_total = ms_since(t_start);
     return ix;

@@ -15,6 +15,20 @@ namespace cobsg {
             throw ::cobsg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));   \
     } while (0)
 
+// RAII CUDA event (destroyed on every exit path).
+struct Event {
+    cudaEvent_t e = nullptr;
+    explicit Event(unsigned flags = cudaEventDefault) {
+        COBS_CUDA(cudaEventCreateWithFlags(&e, flags));
+    }
+    ~Event() {
+        if (e) cudaEventDestroy(e);
+    }
+    Event(const Event&) = delete;
+    Event& operator=(const Event&) = delete;
+    operator cudaEvent_t() const { return e; }
+};
+
 // One block of the device-resident index.  Rows are re-pitched to a 32-byte
 // multiple so a warp's 128-byte column slice never straddles an extra DRAM
 // sector; bytes [row_bytes, pitch) of every row are zero.

@@ -231,9 +231,7 @@ std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint6
     PinnedBuf stage[2];
     stage[0].reserve(kStage);
     stage[1].reserve(kStage);
-    cudaEvent_t done[2];
-    COBS_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
-    COBS_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
     int cur = 0;
     bool used[2] = {false, false};
     for (size_t b = 0; b < ix->blocks.size(); ++b) {
@@ -258,8 +256,6 @@ std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint6
         }
     }
     COBS_CUDA(cudaStreamSynchronize(ix->stream));
-    cudaEventDestroy(done[0]);
-    cudaEventDestroy(done[1]);
     ix->finish_upload();
     return ix;
 }

@@ -630,9 +630,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     const uint64_t wtot = win_base[n];
     const uint64_t pat_bytes = h_off[n] - h_off[0];
 
-    cudaEvent_t ev_begin, ev_end;
-    COBS_CUDA(cudaEventCreate(&ev_begin));
-    COBS_CUDA(cudaEventCreate(&ev_end));
+    Event ev_begin, ev_end;
     COBS_CUDA(cudaEventRecord(ev_begin, st));
 
     // Buffers
@@ -663,8 +661,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     COBS_CUDA(cudaMemcpyAsync(ws.win_base.ptr, win_base.data(), 8 * (n + 1), cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(ws.tab_off.ptr, tab_off.data(), 8 * n, cudaMemcpyHostToDevice, st));
 
-    cudaEvent_t ev[4];
-    for (auto& e : ev) COBS_CUDA(cudaEventCreate(&e));
+    Event ev[4];
     COBS_CUDA(cudaEventRecord(ev[0], st));
 
     // kernel 1
@@ -893,9 +890,6 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     float ttot = 0;
     cudaEventElapsedTime(&ttot, ev_begin, ev_end);
     R.ms_total = ttot;
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaEventDestroy(ev_begin);
-    cudaEventDestroy(ev_end);
 }
 
 } // namespace cobsg
