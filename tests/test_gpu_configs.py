@@ -135,10 +135,18 @@ def test_c5_full_sample(gpu):
         r = rng.randrange(w)
         thr = synth.c5_thr16(w, int(tcs[base:base + dc].max()))
         assert view.row_data(b, r) == synth.c5_row(cfg.seed, b, r, (dc + 7) // 8, thr, dc)
-    ids = np.asarray(sorted(rng.sample(range(cfg.n_queries), 12)), dtype=np.uint64)
+    # the seeded 1 % subsample of the batch (BASELINE.json config 5): dense
+    # scores (threshold-free) and hit lists at K = 0.8
+    ids = np.asarray(sorted(random.Random(0x1F).sample(range(cfg.n_queries), cfg.n_queries // 100)),
+                     dtype=np.uint64)
     qb, qo = synth.queries(cfg, ids)
-    got = cb.query_batch_raw(view, qb, qo, 1e-12, scores=True)
+    got = cb.query_batch_raw(view, qb, qo, 1e-12, scores=True, hits=False)
     ell, sk, st, nh, dense = orc.query_batch(qb, qo, 1e-12, scores=True)
     assert np.array_equal(got.ell.astype(np.uint64), ell)
     assert np.array_equal(got.dense.astype(np.uint32), dense)
+    hits = cb.query_batch_raw(view, qb, qo, cfg.K)
+    tau = np.ceil(cfg.K * ell.astype(np.float64) - 1e-9).astype(np.int64)
+    for i in range(len(ids)):
+        want = int((dense[i] >= max(1, tau[i])).sum())
+        assert int(hits.hit_n[i]) == want
     view.close()
