@@ -116,10 +116,10 @@ __device__ __forceinline__ uint64_t revcomp_code(uint64_t code, uint32_t q) {
 // get their code from the tile (canonical = min(code, revcomp)), XXH64 from
 // the code and an exact code-keyed insert; other windows take the byte path.
 // The distinct terms are compacted in window order.  QC: 31 or 0.
-template <int QC>
-__global__ void __launch_bounds__(kTermizeThreads) termize_hash_kernel(TermizeArgs a) {
+template <int QC, int THREADS>
+__global__ void __launch_bounds__(THREADS) termize_hash_kernel(TermizeArgs a) {
     extern __shared__ __align__(16) unsigned long long s_dyn[];
-    using Reduce = cub::BlockReduce<uint64_t, kTermizeThreads>;
+    using Reduce = cub::BlockReduce<uint64_t, THREADS>;
     __shared__ typename Reduce::TempStorage tmp_reduce;
     __shared__ uint32_t s_count; // distinct terms of the current query
     const uint32_t q = QC ? QC : a.q, k = a.k;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kTermizeThreads) termize_hash_kernel(TermizeAr
             // window r*threads + tid: every thread busy even for short patterns;
             // winners are appended with one shared atomic per warp and round
             // (term order inside the list is irrelevant: scores are sums)
-            for (uint32_t r0 = 0; r0 < nwin; r0 += kTermizeThreads) {
+            for (uint32_t r0 = 0; r0 < nwin; r0 += THREADS) {
                 const uint32_t jl = r0 + threadIdx.x;
                 const bool active = jl < nwin;
                 const uint64_t j = tb + jl;
@@ -685,11 +685,14 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
         if (tab_off[i] == kNoGtab) small_S = std::max(small_S, set_slots(win_base[i + 1] - win_base[i]));
     ta.smem_slots = static_cast<uint32_t>(std::min<uint64_t>(small_S, kSmemSlots));
     size_t smem = static_cast<size_t>(ta.smem_slots) * 8 + kTileBytes;
-    auto k1 = q == 31 ? termize_hash_kernel<31> : termize_hash_kernel<0>;
+    // long patterns (large shared sets, few CTAs per SM) get 1,024 threads
+    const bool wide = smem > (64u << 10);
+    auto k1 = q == 31 ? (wide ? termize_hash_kernel<31, 1024> : termize_hash_kernel<31, kTermizeThreads>)
+                      : (wide ? termize_hash_kernel<0, 1024> : termize_hash_kernel<0, kTermizeThreads>);
     COBS_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     unsigned grid1 = static_cast<unsigned>(std::min<uint64_t>(n, 1u << 30));
-    k1<<<grid1, kTermizeThreads, smem, st>>>(ta);
+    k1<<<grid1, wide ? 1024 : kTermizeThreads, smem, st>>>(ta);
     COBS_CUDA(cudaGetLastError());
     R.launches += 1;
     COBS_CUDA(cudaEventRecord(ev[1], st));
