@@ -8,12 +8,13 @@
 //   host        classic width / compact (term_count, name) sort, blocks of
 //               B, per-block widths        (classic_index.cpp:40-64,
 //               compact_index.cpp:19-52, bloom.cpp:50-66)
-//   fill pass   one thread per window and seed: atomicOr of bit
-//               (XXH64 % w_b, column) into the block's row-major matrix,
-//               written straight into the pitched HBM layout of the query
-//               index (so a built index is queryable in place); the file
-//               payload is its un-pitched D2H copy  (classic_index.cpp:26-36,
-//               bit_matrix.hpp:25-27).  OR is idempotent, so every window is
+//   fill pass   for every window and seed, bit (XXH64 % w_b, column)
+//               (classic_index.cpp:26-36, bit_matrix.hpp:25-27): 32
+//               consecutive columns of a block are one u32 per row, so waves
+//               of such column "slabs" (L2-sized) are filled with atomicOr and
+//               then copied into the pitched HBM layout of the query index
+//               (a built index is queryable in place; the file payload is its
+//               un-pitched D2H copy).  OR is idempotent, so every window is
 //               filled, not just the distinct ones.
 #include <algorithm>
 #include <chrono>
@@ -141,55 +142,85 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
     }
 }
 
-struct FillBlock {
-    uint64_t base; // byte offset of row 0 in the pitched payload
-    uint64_t w, magic, rb; // rb: row stride (the device pitch)
+// ---- slab fill: the bits of 32 consecutive columns of a block are one u32
+// per row -- a dense "slab" of w words.  A wave of such slabs (sized to stay
+// L2-resident) is filled with atomicOr, then copied into the matrix's 4-byte
+// column positions (one strided u32 store per row), instead of random
+// read-modify-writes straight into the whole (HBM-sized) matrix.
+
+struct SlabDoc {
+    uint64_t run_lo, seg_lo, seg_hi; // first run and segment range of the document
+    uint64_t slab;                   // u32 index of its slab's row 0 in the wave buffer
+    uint64_t w, magic;
+    uint32_t bit;                    // column % 32
+};
+struct SlabGroup {
+    uint64_t src;   // u32 index of row 0 in the wave buffer
+    uint64_t dst;   // payload byte offset of (row 0, byte 4 * group)
+    uint64_t w;
+    uint32_t pitch;
 };
 
 template <int QC>
-__global__ void __launch_bounds__(256) fill_kernel(WinArgs a, const FillBlock* blocks,
-                                                   const uint32_t* doc_block, const uint32_t* doc_col,
-                                                   unsigned int* words) {
+__global__ void __launch_bounds__(256) slab_fill_kernel(WinArgs a, const SlabDoc* docs,
+                                                        const uint64_t* run_prefix, uint32_t ndocs,
+                                                        unsigned int* slab) {
     const uint32_t q = QC ? QC : a.q;
-    __shared__ uint64_t s_seg[2];
-    const uint64_t nchunks = (a.r_hi - a.r_lo + kChunkRuns - 1) / kChunkRuns;
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const uint64_t r0 = a.r_lo + c * kChunkRuns, r1 = min(a.r_hi, r0 + kChunkRuns);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        s_seg[0] = find_seg(a, r0);
-        s_seg[1] = find_seg(a, r1 - 1) + 1;
-    }
-    __syncthreads();
-    const uint64_t slo = s_seg[0], shi = s_seg[1];
-    for (uint64_t g = r0 + threadIdx.x; g < r1; g += blockDim.x) {
-        const uint64_t s = find_seg_in(a, g, slo, shi);
-        const uint32_t doc = a.seg_doc[s];
+    const uint64_t total = run_prefix[ndocs];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = ndocs; // run_prefix[lo] <= t < run_prefix[hi]
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (run_prefix[mid] <= t)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const SlabDoc D = docs[lo];
+        const uint64_t g = D.run_lo + (t - run_prefix[lo]);
+        const uint64_t s = find_seg_in(a, g, D.seg_lo, D.seg_hi);
         const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
         const uint64_t W = len >= q ? len - q + 1 : 0;
         const uint64_t j0 = (g - a.seg_rbase[s]) * kBRun;
         const uint64_t j1 = min(W, j0 + kBRun);
         const uint8_t* sb = a.seqs + a.seg_off[s];
-        const FillBlock B = blocks[doc_block[doc]];
-        const uint32_t col = doc_col[doc];
-        const uint64_t colbyte = B.base + (col >> 3);
-        auto set_bit = [&](uint64_t h) { // bit (h % w, col): bit_matrix.hpp:25-27
-            const uint64_t byte = colbyte + fastmod(h, B.w, B.magic) * B.rb;
-            atomicOr(words + (byte >> 2), 1u << (((byte & 3) << 3) + (col & 7)));
-        };
+        unsigned int* col = slab + D.slab;
+        const unsigned int bit = 1u << D.bit;
         roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
             const uint8_t* w = sb + j;
             if (dna) {
-                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_code<QC>(code, q, seed));
+                for (uint32_t seed = 0; seed < a.k; ++seed)
+                    atomicOr(col + fastmod(xxh64_code<QC>(code, q, seed), D.w, D.magic), bit);
             } else if (a.canonical) {
                 if (q <= 32 || !window_acgt(w, q)) return;
                 const bool rc = choose_rc(w, q);
-                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_term(w, q, rc, seed));
+                for (uint32_t seed = 0; seed < a.k; ++seed)
+                    atomicOr(col + fastmod(xxh64_term(w, q, rc, seed), D.w, D.magic), bit);
             } else {
-                for (uint32_t seed = 0; seed < a.k; ++seed) set_bit(xxh64_term(w, q, false, seed));
+                for (uint32_t seed = 0; seed < a.k; ++seed)
+                    atomicOr(col + fastmod(xxh64_term(w, q, false, seed), D.w, D.magic), bit);
             }
         });
     }
+}
+
+__global__ void slab_copy_kernel(const SlabGroup* groups, const uint64_t* row_prefix, uint32_t ngroups,
+                                 const unsigned int* slab, uint8_t* payload) {
+    const uint64_t total = row_prefix[ngroups];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = ngroups;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (row_prefix[mid] <= t)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const SlabGroup G = groups[lo];
+        const uint64_t r = t - row_prefix[lo];
+        *reinterpret_cast<unsigned int*>(payload + G.dst + r * G.pitch) = slab[G.src + r];
     }
 }
 
@@ -361,7 +392,6 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         B = P.block_size;
     }
     const uint64_t nb = (n_docs + B - 1) / B;
-    std::vector<uint32_t> doc_block(n_docs), doc_col(n_docs);
     for (uint64_t b = 0; b < nb; ++b) {
         uint64_t lo = b * B, hi = std::min(n_docs, lo + B), mx = 0;
         BlockMeta bm;
@@ -370,8 +400,6 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             uint64_t d = order[i];
             meta.docs.push_back({names[d], tc[d]});
             mx = std::max(mx, tc[d]);
-            doc_block[d] = static_cast<uint32_t>(b);
-            doc_col[d] = static_cast<uint32_t>(i - lo);
         }
         bm.w = (kind == kKindClassic && forced_w != 0) ? forced_w : bloom::size_filter(mx, P.p, P.k);
         meta.blocks.push_back(bm);
@@ -386,31 +414,86 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     ix->allocate(); // refuses a matrix that does not fit in free HBM
     COBS_CUDA(cudaMemsetAsync(ix->payload, 0, ix->payload_bytes, ix->stream));
     COBS_CUDA(cudaStreamSynchronize(ix->stream));
-    std::vector<FillBlock> fb(nb);
-    for (uint64_t b = 0; b < nb; ++b) {
-        fb[b].base = ix->blocks[b].base;
-        fb[b].w = ix->blocks[b].w;
-        fb[b].magic = ix->blocks[b].magic;
-        fb[b].rb = ix->blocks[b].pitch; // row stride on the device
-    }
-    DevBuf d_fb, d_dblock, d_dcol;
-    d_fb.reserve(sizeof(FillBlock) * nb);
-    d_dblock.reserve(4 * n_docs);
-    d_dcol.reserve(4 * n_docs);
-    COBS_CUDA(cudaMemcpyAsync(d_fb.ptr, fb.data(), sizeof(FillBlock) * nb, cudaMemcpyHostToDevice, st));
-    COBS_CUDA(cudaMemcpyAsync(d_dblock.ptr, doc_block.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
-    COBS_CUDA(cudaMemcpyAsync(d_dcol.ptr, doc_col.data(), 4 * n_docs, cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaEventRecord(e2, st));
     wa.seg_lo = 0;
     wa.seg_hi = n_segs;
-    wa.r_lo = 0;
-    wa.r_hi = total_runs;
     if (total_runs > 0) {
-        auto fk = q == 31 ? fill_kernel<31> : fill_kernel<0>;
-        fk<<<148 * 16, 256, 0, st>>>(wa, d_fb.as<FillBlock>(), d_dblock.as<uint32_t>(),
-                                              d_dcol.as<uint32_t>(),
-                                              reinterpret_cast<unsigned int*>(ix->payload));
-        COBS_CUDA(cudaGetLastError());
+        // waves of whole 32-column groups, block-major, slabs <= wave_bytes
+        std::vector<SlabDoc> sdocs;
+        std::vector<uint64_t> run_prefix;   // per wave: ndocs+1 entries (concatenated)
+        std::vector<SlabGroup> sgroups;
+        std::vector<uint64_t> row_prefix;   // per wave: ngroups+1 entries (concatenated)
+        struct Wave { size_t doc0, ndocs, rp0, grp0, ngroups, gp0; uint64_t words; };
+        std::vector<Wave> waves;
+        Wave cur{0, 0, 0, 0, 0, 0, 0};
+        uint64_t max_words = 0;
+        auto close_wave = [&] {
+            if (cur.ngroups == 0) return;
+            max_words = std::max(max_words, cur.words);
+            waves.push_back(cur);
+            cur = Wave{sdocs.size(), 0, run_prefix.size(), sgroups.size(), 0, row_prefix.size(), 0};
+        };
+        const uint64_t wave_words = std::max<uint64_t>(wave_bytes / 4, 1);
+        for (uint64_t b = 0; b < nb; ++b) {
+            const DevBlock& d = ix->blocks[b];
+            const uint64_t ngr = (d.dc + 31) / 32;
+            for (uint64_t gi = 0; gi < ngr; ++gi) {
+                if (cur.ngroups > 0 && cur.words + d.w > wave_words) close_wave();
+                if (cur.ngroups == 0) { // open: prefix starts
+                    cur.rp0 = run_prefix.size();
+                    cur.gp0 = row_prefix.size();
+                    run_prefix.push_back(0);
+                    row_prefix.push_back(0);
+                }
+                SlabGroup G{cur.words, d.base + 4 * gi, d.w, d.pitch};
+                sgroups.push_back(G);
+                row_prefix.push_back(row_prefix.back() + d.w);
+                for (uint64_t c = 32 * gi; c < std::min<uint64_t>(d.dc, 32 * gi + 32); ++c) {
+                    const uint64_t doc = order[d.doc_base + c];
+                    SlabDoc D{};
+                    D.seg_lo = doc_segs[doc];
+                    D.seg_hi = doc_segs[doc + 1];
+                    D.run_lo = seg_rbase[D.seg_lo];
+                    D.slab = cur.words;
+                    D.w = d.w;
+                    D.magic = d.magic;
+                    D.bit = static_cast<uint32_t>(c % 32);
+                    sdocs.push_back(D);
+                    run_prefix.push_back(run_prefix.back() + (seg_rbase[D.seg_hi] - D.run_lo));
+                    ++cur.ndocs;
+                }
+                cur.words += d.w;
+                ++cur.ngroups;
+            }
+        }
+        close_wave();
+        DevBuf d_sdocs, d_rp, d_sgroups, d_gp, d_slab;
+        d_sdocs.reserve(sizeof(SlabDoc) * std::max<size_t>(sdocs.size(), 1));
+        d_rp.reserve(8 * run_prefix.size());
+        d_sgroups.reserve(sizeof(SlabGroup) * std::max<size_t>(sgroups.size(), 1));
+        d_gp.reserve(8 * row_prefix.size());
+        d_slab.reserve(4 * std::max<uint64_t>(max_words, 1));
+        COBS_CUDA(cudaMemcpyAsync(d_sdocs.ptr, sdocs.data(), sizeof(SlabDoc) * sdocs.size(), cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_rp.ptr, run_prefix.data(), 8 * run_prefix.size(), cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_sgroups.ptr, sgroups.data(), sizeof(SlabGroup) * sgroups.size(),
+                                  cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_gp.ptr, row_prefix.data(), 8 * row_prefix.size(), cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaEventRecord(e2, st));
+        auto fk = q == 31 ? slab_fill_kernel<31> : slab_fill_kernel<0>;
+        for (const Wave& wv : waves) {
+            COBS_CUDA(cudaMemsetAsync(d_slab.ptr, 0, 4 * wv.words, st));
+            const uint64_t runs = run_prefix[wv.rp0 + wv.ndocs];
+            if (runs > 0)
+                fk<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (runs + 255) / 256)), 256, 0, st>>>(
+                    wa, d_sdocs.as<SlabDoc>() + wv.doc0, d_rp.as<uint64_t>() + wv.rp0,
+                    static_cast<uint32_t>(wv.ndocs), d_slab.as<unsigned int>());
+            slab_copy_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (wv.words + 255) / 256)), 256, 0,
+                               st>>>(d_sgroups.as<SlabGroup>() + wv.grp0, d_gp.as<uint64_t>() + wv.gp0,
+                                     static_cast<uint32_t>(wv.ngroups), d_slab.as<unsigned int>(), ix->payload);
+            COBS_CUDA(cudaGetLastError());
+        }
+        COBS_CUDA(cudaEventRecord(e3, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
     }
     COBS_CUDA(cudaEventRecord(e3, st));
     COBS_CUDA(cudaStreamSynchronize(st));
