@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
             roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
                 const uint8_t* w = sb + j;
                 const uint32_t pos = static_cast<uint32_t>(w - dbase);
-                if (dna) {
-                    cnt += set_insert_code(t, mask, xxh64_code<QC>(code, q, 0), code);
+                if (dna) { // the slot only needs a well-mixed hash of the exact code
+                    cnt += set_insert_code(t, mask, mix_code(code), code);
                 } else if (a.canonical) {
                     if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
                     const bool rc = choose_rc(w, q);
@@ -326,11 +326,15 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     // (random CAS into L2-resident sets instead of DRAM; a document larger
     // than a wave gets a wave of its own)
     std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
-    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] + doc_w[d] / 2 + 1);
+    uint64_t load_div = 4; // slots >= load_div/2 * windows (load <= 2/load_div)
+    if (const char* e = std::getenv("COBS_COUNT_LOAD_DIV")) load_div = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
+    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] * load_div / 2 + 1);
     size_t free_b = 0, total_b = 0;
     COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    uint64_t wave_bytes = 96ull << 20;
+    uint64_t wave_bytes = 192ull << 20;
     if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
+    uint64_t slab_wave_bytes = 96ull << 20;
+    if (const char* e = std::getenv("COBS_SLAB_WAVE_MB")) slab_wave_bytes = std::strtoull(e, nullptr, 10) << 20;
     const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
     std::vector<uint64_t> wave_lo{0};
     uint64_t max_slots = 0;
@@ -433,7 +437,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             waves.push_back(cur);
             cur = Wave{sdocs.size(), 0, run_prefix.size(), sgroups.size(), 0, row_prefix.size(), 0};
         };
-        const uint64_t wave_words = std::max<uint64_t>(wave_bytes / 4, 1);
+        const uint64_t wave_words = std::max<uint64_t>(slab_wave_bytes / 4, 1);
         for (uint64_t b = 0; b < nb; ++b) {
             const DevBlock& d = ix->blocks[b];
             const uint64_t ngr = (d.dc + 31) / 32;

@@ -292,6 +292,16 @@ struct Roller {
     __device__ __forceinline__ uint64_t canon() const { return fwd < rev ? fwd : rev; }
 };
 
+// Slot hash for code-keyed sets where the XXH64 row hash is not needed
+// (the splitmix64 finaliser: two multiplies).
+__device__ __forceinline__ uint64_t mix_code(uint64_t z) {
+    z ^= z >> 31;
+    z *= 0x7FB5D329728EA185ULL;
+    z ^= z >> 27;
+    z *= 0x81DADEF4BC2DD44DULL;
+    return z ^ (z >> 33);
+}
+
 // Exact set insert keyed by the 2-bit code (bit 63 clear; +1 keeps 0 empty).
 // Byte-path keys (set_insert above) always have bit 63 set when both kinds
 // share a table (see set_insert_tagged), so the key spaces never collide.

@@ -40,7 +40,7 @@ def column_bits(img: bytes, idx: O.OracleIndex, block: int, col: int) -> np.ndar
     return (rows[:, col // 8] >> (col % 8)) & 1
 
 
-def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0):
+def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0, repeat: int = 1):
     cfg = synth.CONFIGS[name]
     if n_queries:
         cfg = synth.replace(cfg, n_queries=n_queries)
@@ -59,10 +59,13 @@ def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0
     params = cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p, canonical=cfg.canonical,
                             block_size=cfg.block_size)
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    view, _ = cb.build_device(dev.data_ptr(), seg_off, doc_segs, names, params, cfg.kind,
-                              seqs_on_device=True)
-    wall = time.perf_counter() - t
+    for rep in range(repeat):  # the last build is reported (earlier ones warm up)
+        if rep:
+            view.close()
+        t = time.perf_counter()
+        view, _ = cb.build_device(dev.data_ptr(), seg_off, doc_segs, names, params, cfg.kind,
+                                  seqs_on_device=True)
+        wall = time.perf_counter() - t
     c, f, tot = cb.last_build_timing()
     res["build"] = {"ms_count": c, "ms_fill": f, "ms_total_call": tot, "wall_s": wall,
                     "docs_per_s_kernels": cfg.n_docs / ((c + f) / 1e3),
@@ -151,10 +154,11 @@ def main():
     ap.add_argument("--docs", type=int, default=4)
     ap.add_argument("--queries", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--repeat", type=int, default=1)
     a = ap.parse_args()
     results = []
     for c in a.configs:
-        r = run(c, a.docs, a.queries, a.batch)
+        r = run(c, a.docs, a.queries, a.batch, a.repeat)
         print(json.dumps(r), flush=True)
         results.append(r)
         json.dump(results, open(a.out, "w"), indent=1)
