@@ -46,6 +46,7 @@ struct WinArgs {
     uint64_t r_lo, r_hi;       // run range of this pass
     uint32_t q, k;
     int canonical;
+    uint32_t tag_mask; // all ones (tests may narrow it to force tag collisions)
 };
 
 // run g -> segment (seg_rbase[s] <= g < seg_rbase[s+1]), searched in [lo, hi)
@@ -125,11 +126,11 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
                 } else if (a.canonical) {
                     if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
                     const bool rc = choose_rc(w, q);
-                    cnt += set_insert(t, mask, xxh64_term(w, q, rc, 0), pos, dbase, q, true, rc);
+                    cnt += set_insert(t, mask, xxh64_term(w, q, rc, 0), pos, dbase, q, true, rc, a.tag_mask);
                 } else {
                     const uint64_t h = xxh64_term(w, q, false, 0);
-                    cnt += q <= 32 ? set_insert_tagged(t, mask, h, pos, dbase, q)
-                                   : set_insert(t, mask, h, pos, dbase, q, false, false);
+                    cnt += q <= 32 ? set_insert_tagged(t, mask, h, pos, dbase, q, a.tag_mask)
+                                   : set_insert(t, mask, h, pos, dbase, q, false, false, a.tag_mask);
                 }
             });
         }
@@ -319,6 +320,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     wa.q = q;
     wa.k = P.k;
     wa.canonical = P.canonical ? 1 : 0;
+    wa.tag_mask = debug_tag_mask();
 
     Event e0, e1, e2, e3;
 

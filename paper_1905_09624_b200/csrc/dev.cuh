@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "host.hpp"
@@ -58,6 +59,17 @@ __host__ __device__ __forceinline__ uint64_t fastmod(uint64_t h, uint64_t w, uin
     return r;
 }
 inline uint64_t mod_magic(uint64_t w) { return ~0ULL / w; }
+
+// Tag bits of the byte-path dedup keys: all of them, unless the test-only
+// COBS_DEBUG_TAG_BITS narrows them so distinct terms collide on the tag and
+// the exact byte comparison decides (tests/test_gpu_edge.py).
+inline uint32_t debug_tag_mask() {
+    if (const char* e = std::getenv("COBS_DEBUG_TAG_BITS")) {
+        int b = std::atoi(e);
+        if (b >= 0 && b < 32) return (1u << b) - 1u;
+    }
+    return 0xffffffffu;
+}
 
 // ---- XXH64 (FORMAT.md "Term hashing"; reference xxhash64.hpp:45-95) ----
 
@@ -164,8 +176,9 @@ __device__ __forceinline__ bool terms_equal(const uint8_t* a, bool rca, const ui
 // distinct terms.  Returns true iff this window owns a new slot.
 __device__ __forceinline__ bool set_insert(unsigned long long* tab, uint64_t mask, uint64_t h,
                                            uint32_t pos, const uint8_t* win_base, uint32_t q,
-                                           bool canonical, bool rc) {
-    unsigned long long key = ((unsigned long long)(h >> 32) << 32) | (unsigned long long)(pos + 1u);
+                                           bool canonical, bool rc, uint32_t tag_mask = 0xffffffffu) {
+    // tag_mask < all-ones only in tests: forces tag collisions onto the byte compare
+    unsigned long long key = ((unsigned long long)((h >> 32) & tag_mask) << 32) | (unsigned long long)(pos + 1u);
     uint64_t slot = h & mask;
     const uint8_t* mine = win_base + pos;
     for (;;) {
@@ -323,8 +336,10 @@ __device__ __forceinline__ bool set_insert_code(unsigned long long* tab, uint64_
 // Byte-path insert for tables shared with code keys: key bit 63 set, 31-bit
 // hash tag, 32-bit position+1; equal tags are resolved by the window bytes.
 __device__ __forceinline__ bool set_insert_tagged(unsigned long long* tab, uint64_t mask, uint64_t h,
-                                                  uint32_t pos, const uint8_t* win_base, uint32_t q) {
-    const unsigned long long key = (1ull << 63) | ((unsigned long long)((h >> 33) & 0x7fffffffu) << 32) |
+                                                  uint32_t pos, const uint8_t* win_base, uint32_t q,
+                                                  uint32_t tag_mask = 0xffffffffu) {
+    const unsigned long long key = (1ull << 63) |
+                                   ((unsigned long long)((h >> 33) & 0x7fffffffu & tag_mask) << 32) |
                                    (unsigned long long)(pos + 1u);
     uint64_t slot = h & mask;
     const uint8_t* mine = win_base + pos;

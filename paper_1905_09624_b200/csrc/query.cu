@@ -51,6 +51,7 @@ struct TermizeArgs {
     int canonical;
     double K;
     uint32_t smem_slots; // shared-memory set capacity (tile arrays follow it)
+    uint32_t tag_mask;   // all ones (tests may narrow it to force tag collisions)
     uint64_t* hashes; // [win_total * k]
     uint32_t* ell;
     uint64_t* skipped;
@@ -198,14 +199,16 @@ __global__ void __launch_bounds__(THREADS) termize_hash_kernel(TermizeArgs a) {
                             rc = choose_rc(w, q);
                             h = xxh64_term(w, q, rc, 0);
                             bytep = true;
-                            won = set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, true, rc);
+                            won = set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, true, rc,
+                                             a.tag_mask);
                         }
                     } else { // raw bytes (any alphabet): termizer.cpp:120-122
                         h = xxh64_term(w, q, false, 0);
                         bytep = true;
                         won = code_path
-                                  ? set_insert_tagged(tab, S - 1, h, static_cast<uint32_t>(j), pat, q)
-                                  : set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, false, false);
+                                  ? set_insert_tagged(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, a.tag_mask)
+                                  : set_insert(tab, S - 1, h, static_cast<uint32_t>(j), pat, q, false, false,
+                                               a.tag_mask);
                     }
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, won);
@@ -676,6 +679,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ta.k = k;
     ta.canonical = P.canonical ? 1 : 0;
     ta.K = K;
+    ta.tag_mask = debug_tag_mask();
     ta.hashes = ws.hashes.as<uint64_t>();
     ta.ell = ws.ell.as<uint32_t>();
     ta.skipped = ws.skipped.as<uint64_t>();

@@ -84,3 +84,23 @@ def test_exact_integer_thresholds(gpu):
     # patterns with l = 10, 20, 30, 100, 1000 distinct 31-mers
     pats = [base[:31 + ell - 1] for ell in (10, 20, 30, 100, 1000)]
     check(img, pats, Ks=(0.9, 0.1, 0.3, 0.7, 1.0), tops=(0,))
+
+
+def test_forced_tag_collisions_stay_exact(gpu):
+    """With the dedup tags narrowed to 2 bits (COBS_DEBUG_TAG_BITS, read per
+    call), distinct byte-path terms collide on the tag all the time and the
+    exact byte comparison must keep l, term counts and scores right."""
+    import os
+    rng = random.Random(77)
+    docs = [(b"p%03d" % i, [rb(rng, rng.randint(50, 900), b"ACDEFGHIKLMNPQRSTVWY")]) for i in range(25)]
+    dna = [(b"q%03d" % i, [rb(rng, rng.randint(50, 900), b"ACGTN")]) for i in range(25)]
+    os.environ["COBS_DEBUG_TAG_BITS"] = "2"
+    try:
+        for corpus, q, canonical in [(docs, 10, False), (dna, 40, True), (dna, 31, False)]:
+            img = O.build_image(corpus, q=q, k=2, canonical=canonical, block_size=6, kind=1)
+            assert cb.build_image(corpus, cb.IndexParams(q=q, k=2, canonical=canonical, block_size=6), 1,
+                                  device=0) == img
+            pats = [corpus[i][1][0][: 60 + 10 * i] for i in range(len(corpus))]
+            check(img, pats, Ks=(1e-12, 0.5), tops=(0,))
+    finally:
+        del os.environ["COBS_DEBUG_TAG_BITS"]
