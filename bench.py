@@ -336,10 +336,14 @@ def run_gpu(args):
         ms = reduce_max(e0.elapsed_time(e1) / steps, f"cuda:{local}")  # max over ranks
         return ms, outs
 
+    def step_pruned():
+        return cb.query_batch_raw(view, h_pat.numpy(), h_off.numpy().view(np.uint64), cfg.K, prune=True)
+
     clocks = ClockSampler(local)
     clocks.start()
     ms_dev, outs = timed(step_device, args.steps, args.warmup)
     ms_e2e, outs_e2e = timed(step_e2e, args.steps, 1)
+    ms_pruned, outs_pruned = timed(step_pruned, args.steps, 1)
     clk = clocks.stop()
 
     grams = int(outs[-1].ell.astype(np.uint64).sum())
@@ -402,6 +406,15 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
             "gpu_launches": int(sum(o.launches for o in outs)),
+            # the same batch with threshold pruning (COBS_Q_PRUNE): a (query,
+            # slice) stops reading rows once no document there can reach tau;
+            # identical hit lists (checked here and in the tests), fewer bytes.
+            # Not used for `value`: the headline keeps the reference's full work.
+            "pruned": {"e2e_value": total_grams / (ms_pruned / 1e3), "unit": UNIT,
+                       "ms_per_step": ms_pruned,
+                       "gather_ms": statistics.mean(o.ms_gather for o in outs_pruned),
+                       "hits_identical": bool(np.array_equal(outs_pruned[-1].docs, outs_e2e[-1].docs)
+                                              and np.array_equal(outs_pruned[-1].hit_n, outs_e2e[-1].hit_n))},
             "roofline": roofline,
             "cpu_baseline": cpu_base,
             "build": build,

@@ -127,6 +127,9 @@ int cobs_gpu_index_image(const cobs_gpu_index* index, uint8_t** image, uint64_t*
 #define COBS_Q_SCORES 2u        /* dense per-document score matrix n x total_docs */
 #define COBS_Q_DEVICE_INPUT 4u  /* patterns / offsets are device pointers */
 #define COBS_Q_KEEP_DEVICE 8u   /* leave results in HBM (no D2H); for timing */
+#define COBS_Q_PRUNE 16u        /* hits only: stop reading a (query, slice)'s rows once no
+                                   document there can still reach tau; identical hit lists,
+                                   fewer row bytes (not in the reference) */
 
 /* Replaces cobs::query (proj/include/cobs/query.hpp:46-47,
  * proj/src/query.cpp:123-164) over a batch, the way the CLI batch mode

@@ -292,7 +292,7 @@ def pack_patterns(patterns: Sequence[bytes]) -> Tuple[np.ndarray, np.ndarray]:
 
 def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: int = 0,
                     scores: bool = False, hits: bool = True, device_input: bool = False,
-                    keep_device: bool = False) -> BatchResult:
+                    keep_device: bool = False, prune: bool = False) -> BatchResult:
     """Batched cobs::query over packed patterns.  ``buf``/``offsets`` are
     numpy arrays (host) or integer device addresses with device_input."""
     n = (len(offsets) - 1) if not device_input else int(offsets[1])
@@ -307,6 +307,8 @@ def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: 
         flags |= N.Q_DEVICE_INPUT
     if keep_device:
         flags |= N.Q_KEEP_DEVICE
+    if prune:
+        flags |= N.Q_PRUNE
     r = C.c_void_p()
     err = _errbuf()
     rc = N.lib.cobs_gpu_query_batch(view._h, pbuf, poff, n, K, top_t, flags, C.byref(r), err,

@@ -112,5 +112,5 @@ for _name, (_res, _args) in SIGNATURES.items():
     _sig(_name, _res, _args)
 
 OK, EUSAGE, EDATA, ECUDA = 0, 1, 2, 4
-Q_HITS, Q_SCORES, Q_DEVICE_INPUT, Q_KEEP_DEVICE = 1, 2, 4, 8
+Q_HITS, Q_SCORES, Q_DEVICE_INPUT, Q_KEEP_DEVICE, Q_PRUNE = 1, 2, 4, 8, 16
 B_DEVICE_INPUT = 1

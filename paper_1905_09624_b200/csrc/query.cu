@@ -258,6 +258,7 @@ struct GatherArgs {
     uint64_t D;
     void* scores; // dense [n][D] (uint16 or uint32) or null
     int want_hits;
+    int prune;    // threshold pruning (hits only, no dense scores)
     uint32_t* hit_count; // per query
     unsigned long long* hit_total;
     uint64_t hit_cap;
@@ -311,6 +312,22 @@ __device__ __forceinline__ uint32_t extract(const uint32_t (&F)[NT], int i) {
 #pragma unroll
     for (int p = 0; p < NT; ++p) s |= ((F[p] >> i) & 1u) << p;
     return s;
+}
+
+// Bit-sliced F >= T over the 32 documents of a lane at once.
+template <int NT>
+__device__ __forceinline__ uint32_t ge_mask(const uint32_t (&F)[NT], uint32_t T) {
+    uint32_t gt = 0, eq = 0xffffffffu;
+#pragma unroll
+    for (int p = NT - 1; p >= 0; --p) {
+        const uint32_t tb = ((T >> p) & 1u) ? 0xffffffffu : 0u;
+        gt |= eq & F[p] & ~tb;
+        eq &= ~(F[p] ^ tb);
+    }
+    if constexpr (NT < 32) {
+        if ((T >> NT) != 0u) return 0u; // T beyond the representable counts
+    }
+    return gt | eq;
 }
 
 // Harley-Seal step: 16 document masks into the carry-save accumulators;
@@ -464,26 +481,42 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
             carry = c;
         }
     };
-    uint32_t t0 = 0;
-    for (; t0 + CH <= ell; t0 += CH) chunk(t0, std::false_type{});
-    if (t0 < ell) chunk(t0, std::true_type{});
-    // Flush the carry-save state into plain bit planes F (weight 2^p).
-    uint32_t F[NT];
-#pragma unroll
-    for (int p = 0; p < LCH; ++p) F[p] = 0;
-#pragma unroll
-    for (int p = 0; p < NPP; ++p) F[p + LCH] = P[p];
-    if constexpr (CH == 32) add_at<NT>(F, 4, sixteens);
-    add_at<NT>(F, 3, eights);
-    add_at<NT>(F, 2, fours);
-    add_at<NT>(F, 1, twos);
-    add_at<NT>(F, 0, ones);
-
     // Documents d < dc only: padding columns never count (query.cpp:84-86).
     const uint32_t d0 = slice * 1024u + lane * 32u; // this lane's first document
     uint32_t valid = 0;
     if (d0 < B.dc) valid = (B.dc - d0 >= 32u) ? 0xffffffffu : ((1u << (B.dc - d0)) - 1u);
     const uint64_t gdoc0 = static_cast<uint64_t>(B.doc_base) + d0;
+    const uint32_t tau = a.tau[qi];
+    // Flush the carry-save state into plain bit planes F (weight 2^p).
+    uint32_t F[NT];
+    auto flush = [&]() {
+#pragma unroll
+        for (int p = 0; p < LCH; ++p) F[p] = 0;
+#pragma unroll
+        for (int p = 0; p < NPP; ++p) F[p + LCH] = P[p];
+        if constexpr (CH == 32) add_at<NT>(F, 4, sixteens);
+        add_at<NT>(F, 3, eights);
+        add_at<NT>(F, 2, fours);
+        add_at<NT>(F, 1, twos);
+        add_at<NT>(F, 0, ones);
+    };
+
+    uint32_t t0 = 0;
+    for (; t0 + CH <= ell; t0 += CH) {
+        chunk(t0, std::false_type{});
+        // Optional threshold pruning (hits only): every 2 chunks, if no document
+        // of this slice can still reach tau with all remaining terms, its hit
+        // list is empty whatever those rows hold -- stop reading them.
+        if (a.prune && ((t0 / CH) & 1u) == 1u) {
+            const uint32_t rem = ell - (t0 + CH);
+            if (tau > rem) {
+                flush();
+                if (!__any_sync(0xffffffffu, ge_mask<NT>(F, tau - rem) & valid)) return;
+            }
+        }
+    }
+    if (t0 < ell) chunk(t0, std::true_type{});
+    flush();
 
     if (a.scores) {
         if (NT <= 16) {
@@ -498,18 +531,7 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
     }
     if (!a.want_hits) return;
     // Bit-sliced F >= tau over all 32 documents of the lane at once.
-    const uint32_t tau = a.tau[qi];
-    uint32_t gt = 0, eq = 0xffffffffu;
-#pragma unroll
-    for (int p = NT - 1; p >= 0; --p) {
-        uint32_t tb = ((tau >> p) & 1u) ? 0xffffffffu : 0u;
-        gt |= eq & F[p] & ~tb;
-        eq &= ~(F[p] ^ tb);
-    }
-    if constexpr (NT < 32) {
-        if ((tau >> NT) != 0u) gt = eq = 0; // unreachable: tau <= l < 2^NT
-    }
-    uint32_t hits = (gt | eq) & valid;
+    uint32_t hits = ge_mask<NT>(F, tau) & valid;
     uint32_t cnt = __popc(hits);
     uint32_t incl = cnt;
 #pragma unroll
@@ -734,6 +756,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     ga.D = D;
     ga.scores = want_scores ? ws.scores.ptr : nullptr;
     ga.want_hits = want_hits ? 1 : 0;
+    ga.prune = ((flags & COBS_Q_PRUNE) && want_hits && !want_scores) ? 1 : 0;
     ga.hit_count = ws.hit_count.as<uint32_t>();
     ga.hit_total = ws.hit_total.as<unsigned long long>();
     bool w32 = true;

@@ -338,3 +338,37 @@ def test_streaming_budget_too_small(gpu, tmp_path):
     path = os.path.join(GDIR, "classic_k2.cobs")
     with pytest.raises(cb.DataError, match="more than half the budget"):
         cb.open_random_access(path, 1024, gpu)
+
+
+def test_threshold_pruning_same_hits(gpu):
+    """COBS_Q_PRUNE (stop reading a slice's rows once no document can reach
+    tau) returns exactly the unpruned hit lists (which equal the oracle's)."""
+    from paper_1905_09624_b200 import synth
+    for cfg in (synth.scaled(synth.CONFIGS["c1"], 300, len_scale=0.05, n_queries=300),
+                synth.scaled(synth.CONFIGS["c2"], 400, len_scale=0.005, n_queries=200)):
+        docs = [(n, [s]) for n, s in zip(synth.doc_names(cfg), _doc_bytes(cfg))]
+        img = cb.build_image(docs, cb.IndexParams(q=cfg.q, k=cfg.k, p=cfg.p), 0, device=gpu)
+        view = cb.open_image(img, gpu)
+        qb, qo = synth.queries(cfg)
+        idx = O.OracleIndex.parse(img)
+        for K, top in [(cfg.K, 0), (0.95, 3), (0.5, 0)]:
+            a = cb.query_batch_raw(view, qb, qo, K, top)
+            b = cb.query_batch_raw(view, qb, qo, K, top, prune=True)
+            assert np.array_equal(a.hit_n, b.hit_n)
+            for i in range(len(qo) - 1):
+                assert gpu_hits(view, a, i) == gpu_hits(view, b, i)
+            for i in range(0, len(qo) - 1, 37):
+                ell, sk, hits, _ = idx.query(qb[int(qo[i]):int(qo[i + 1])].tobytes(), K, top)
+                assert gpu_hits(view, b, i) == [list(h) for h in hits]
+        view.close()
+    # config-5 shape: random queries, many slices pruned early
+    view = cb.synth_c5(3, 5000, 1024, 30000.0, 0.5, 0.3, device=gpu)
+    cfg = synth.replace(synth.CONFIGS["c5"], n_docs=5000, n_queries=500)
+    qb, qo = synth.queries(cfg)
+    pats = [qb[int(qo[i]):int(qo[i + 1])].tobytes() for i in range(len(qo) - 1)]
+    pats[7] = pats[7][:40]  # a short pattern: small l, tau reachable
+    a = cb.query_batch(view, pats, 0.8)
+    b = cb.query_batch_raw(view, *cb.pack_patterns(pats), 0.8, prune=True)
+    assert np.array_equal(a.hit_n, b.hit_n) and np.array_equal(a.docs, b.docs)
+    assert np.array_equal(a.scores, b.scores)
+    view.close()
