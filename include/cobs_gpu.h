@@ -197,6 +197,13 @@ int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_
 
 /* build flags */
 #define COBS_B_DEVICE_INPUT 1u /* `seqs` is a device pointer (seg/doc arrays stay on the host) */
+/* Every segment is one pre-extracted term -- the reference's TermSet input
+ * (termizer.hpp:14-26) to build_classic / build_compact
+ * (classic_index.hpp:37-44, compact_index.hpp:26-27): terms are hashed as
+ * given (no windowing, canonicalisation or skipping), term_count = number of
+ * terms, and a term whose length is not q returns COBS_EUSAGE with the
+ * reference's message (classic_index.cpp:49-56). */
+#define COBS_B_TERMS 2u
 
 /* cobs_gpu_build with flags, optionally returning the built index resident
  * in HBM (`index_out`, ready to query; close with cobs_gpu_index_close)

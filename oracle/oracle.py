@@ -289,6 +289,7 @@ def ref():
         L.ref_build_write.argtypes = [_vp, _vp, _vp, _vp, C.c_size_t, C.c_uint32, C.c_uint32,
                                       C.c_double, C.c_int, _u64, C.c_int, _u64, C.c_uint32,
                                       C.c_char_p, C.c_char_p, C.c_size_t]
+        L.ref_build_terms_write.argtypes = L.ref_build_write.argtypes
         L.ref_open.argtypes = [C.c_char_p, C.POINTER(_vp), C.c_char_p, C.c_size_t]
         L.ref_query_fasta_tsv.argtypes = [_vp, C.c_char_p, C.c_double, _u64, C.POINTER(_vp),
                                           C.c_char_p, C.c_size_t]
@@ -415,6 +416,25 @@ def ref_build_write(docs, path: str, q=31, k=1, p=0.3, canonical=False, block_si
     rc = ref().ref_build_write(ptrs, lens, ds, nm, len(names), q, k, p, 1 if canonical else 0,
                                block_size, kind, forced_w, workers or (os.cpu_count() or 1),
                                path.encode(), err, 1024)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+
+
+def ref_build_terms_write(termsets, path: str, q=31, k=1, p=0.3, canonical=False, block_size=1024,
+                          kind=0, forced_w=0, workers=1):
+    """The reference's build_classic / build_compact over TermSets given as
+    (name, [term, ...]) (terms kept as given) + write_index."""
+    segs, doc_seg, names = [], [0], []
+    for name, terms in termsets:
+        names.append(name)
+        segs.extend(terms)
+        doc_seg.append(len(segs))
+    keep, ptrs, lens = _segs(segs)
+    ds = (C.c_uint64 * len(doc_seg))(*doc_seg)
+    nm = (C.c_char_p * max(len(names), 1))(*names)
+    err = C.create_string_buffer(1024)
+    rc = ref().ref_build_terms_write(ptrs, lens, ds, nm, len(names), q, k, p, 1 if canonical else 0,
+                                     block_size, kind, forced_w, workers, path.encode(), err, len(err))
     if rc:
         raise OracleError(rc, err.value.decode())
 

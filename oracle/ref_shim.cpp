@@ -237,6 +237,33 @@ int ref_build_write(const uint8_t* const* segs, const uint64_t* lens, const uint
     });
 }
 
+// build_classic / build_compact over TermSets given directly (each segment
+// is one term, kept as given: no sort, no dedup), + write_index.
+int ref_build_terms_write(const uint8_t* const* segs, const uint64_t* lens, const uint64_t* doc_seg,
+                          const char* const* names, size_t n_docs, uint32_t q, uint32_t k, double p,
+                          int canonical, uint64_t block_size, int kind, uint64_t forced_w,
+                          uint32_t workers, const char* path, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        cobs::IndexParams params;
+        params.q = q;
+        params.k = k;
+        params.p = p;
+        params.canonical = canonical != 0;
+        params.block_size = block_size;
+        std::vector<cobs::TermSet> docs(n_docs);
+        for (size_t d = 0; d < n_docs; ++d) {
+            docs[d].name = names[d];
+            for (uint64_t s = doc_seg[d]; s < doc_seg[d + 1]; ++s)
+                docs[d].terms.emplace_back(reinterpret_cast<const char*>(segs[s]), lens[s]);
+            docs[d].occurrences = docs[d].terms.size();
+        }
+        if (kind == 0)
+            cobs::write_index(cobs::build_classic(docs, params, workers, forced_w), path);
+        else
+            cobs::write_index(cobs::build_compact(docs, params, workers), path);
+    });
+}
+
 // build_classic over docs [0, split) and [split, n) with a common forced
 // width, merge_classic, write_index (acceptance.cpp criterion 9 shape).
 int ref_merge_write(const uint8_t* const* segs, const uint64_t* lens, const uint64_t* doc_seg,

@@ -463,6 +463,32 @@ def build_device(seqs, seg_off: np.ndarray, doc_segs: np.ndarray, names: Sequenc
     return DeviceIndexView(h.value), image
 
 
+def build_from_terms(termsets: Sequence[Tuple[bytes, Sequence[bytes]]], params: IndexParams,
+                     kind: int, forced_w: int = 0, path: Optional[str] = None,
+                     device: int = 0) -> bytes:
+    """build_classic / build_compact over pre-extracted TermSets
+    (classic_index.hpp:37-44, compact_index.hpp:26-27): each (name, terms)
+    pair is a TermSet; terms are hashed as given and term_count = len(terms).
+    A term whose length is not q raises ValueError with the reference's
+    message (classic_index.cpp:49-56).  Returns the file image."""
+    names, buf, seg_off, doc_segs = _pack_docs(termsets)
+    nm = (C.c_char_p * max(len(names), 1))(*names)
+    img = C.c_void_p()
+    ln = C.c_uint64()
+    err = _errbuf()
+    cp = params._c()
+    rc = N.lib.cobs_gpu_build_ex(buf.ctypes.data, seg_off.ctypes.data, len(seg_off) - 1,
+                                 doc_segs.ctypes.data, nm, len(names), C.byref(cp), kind, forced_w,
+                                 device, N.B_TERMS, str(path).encode() if path else None,
+                                 C.byref(img), C.byref(ln), None, err, len(err))
+    if rc:
+        _raise(rc, err)
+    try:
+        return _take_bytes(img, ln.value)
+    finally:
+        N.lib.cobs_gpu_free(img)
+
+
 def synth_docs_device(seed: int, alpha: int, lengths: np.ndarray, dev_ptr: int, device: int = 0,
                       lo: int = 0, hi: Optional[int] = None) -> None:
     """Generate seeded documents [lo, hi) straight into device memory."""

@@ -243,13 +243,32 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                                                 uint64_t n_segs, const uint64_t* doc_segs,
                                                 const std::vector<std::string>& names, const Params& P,
                                                 uint8_t kind, uint64_t forced_w, int device,
-                                                bool seqs_on_device) {
+                                                bool seqs_on_device, bool terms_input) {
     auto t_start = std::chrono::steady_clock::now();
     g_timing = BuildTiming();
     P.validate();                                             // params.hpp:26-35
     const uint64_t n_docs = names.size();
     if (n_docs == 0) throw DataError("build: no documents"); // classic_index.cpp:44
     if (kind != kKindClassic && kind != kKindCompact) throw UsageError("build: unknown index kind");
+    for (uint64_t d = 0; d < n_docs; ++d)
+        if (doc_segs[d + 1] < doc_segs[d] || doc_segs[d + 1] > n_segs)
+            throw UsageError("build: bad document segment ranges");
+    if (doc_segs[0] != 0 || doc_segs[n_docs] != n_segs)
+        throw UsageError("build: document segment ranges must cover all segments in order");
+    // Pre-extracted terms (one segment = one TermSet entry): the reference's
+    // term-length check, in its order -- input order for classic
+    // (classic_index.cpp:49-56, before the name check), sorted order for
+    // compact (each block re-runs build_classic after the name check,
+    // compact_index.cpp:27-52).
+    auto check_terms = [&](const std::vector<uint64_t>& docs_in_order) {
+        for (uint64_t d : docs_in_order)
+            for (uint64_t s = doc_segs[d]; s < doc_segs[d + 1]; ++s)
+                if (seg_off[s + 1] - seg_off[s] != P.q)
+                    throw UsageError("build: term length != q in document " + names[d]);
+    };
+    std::vector<uint64_t> input_order(n_docs);
+    std::iota(input_order.begin(), input_order.end(), 0);
+    if (terms_input && kind == kKindClassic) check_terms(input_order);
     {
         std::vector<const std::string*> sorted(n_docs);
         for (uint64_t d = 0; d < n_docs; ++d) sorted[d] = &names[d];
@@ -259,11 +278,14 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             if (*sorted[i - 1] == *sorted[i]) // classic_index.cpp:17-22
                 throw DataError("duplicate document name: " + *sorted[i]);
     }
-    for (uint64_t d = 0; d < n_docs; ++d)
-        if (doc_segs[d + 1] < doc_segs[d] || doc_segs[d + 1] > n_segs)
-            throw UsageError("build: bad document segment ranges");
-    if (doc_segs[0] != 0 || doc_segs[n_docs] != n_segs)
-        throw UsageError("build: document segment ranges must cover all segments in order");
+    if (terms_input && kind == kKindCompact) {
+        std::vector<uint64_t> by_count = input_order;
+        std::sort(by_count.begin(), by_count.end(), [&](uint64_t a, uint64_t b) {
+            const uint64_t ta = doc_segs[a + 1] - doc_segs[a], tb = doc_segs[b + 1] - doc_segs[b];
+            return ta != tb ? ta < tb : names[a] < names[b];
+        });
+        check_terms(by_count);
+    }
     const uint32_t q = P.q;
 
     COBS_CUDA(cudaSetDevice(device));
@@ -319,7 +341,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     wa.doc_start = d_docstart.as<uint64_t>();
     wa.q = q;
     wa.k = P.k;
-    wa.canonical = P.canonical ? 1 : 0;
+    wa.canonical = (P.canonical && !terms_input) ? 1 : 0; // terms are hashed as given
     wa.tag_mask = debug_tag_mask();
 
     Event e0, e1, e2, e3;
@@ -327,61 +349,65 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     // ---- count pass, in waves of documents whose sets fit in L2 ---------
     // (random CAS into L2-resident sets instead of DRAM; a document larger
     // than a wave gets a wave of its own)
-    std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
-    uint64_t load_div = 4; // slots >= load_div/2 * windows (load <= 2/load_div)
-    if (const char* e = std::getenv("COBS_COUNT_LOAD_DIV")) load_div = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
-    for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] * load_div / 2 + 1);
-    size_t free_b = 0, total_b = 0;
-    COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    uint64_t wave_bytes = 192ull << 20;
-    if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
     uint64_t slab_wave_bytes = 96ull << 20;
     if (const char* e = std::getenv("COBS_SLAB_WAVE_MB")) slab_wave_bytes = std::strtoull(e, nullptr, 10) << 20;
-    const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
-    std::vector<uint64_t> wave_lo{0};
-    uint64_t max_slots = 0;
-    for (uint64_t d0 = 0; d0 < n_docs;) {
-        uint64_t d1 = d0, slots = 0;
-        while (d1 < n_docs && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
-            tab_off[d1] = slots; // relative to the wave's tables
-            slots += tab_slots[d1];
-            ++d1;
-        }
-        max_slots = std::max(max_slots, slots);
-        wave_lo.push_back(d1);
-        d0 = d1;
-    }
-    d_taboff.reserve(8 * n_docs);
-    d_tabslots.reserve(8 * n_docs);
-    d_tab.reserve(8 * max_slots);
-    COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
-    COBS_CUDA(cudaMemcpyAsync(d_taboff.ptr, tab_off.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
-    COBS_CUDA(cudaEventRecord(e0, st));
-    auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
-    for (size_t wv = 0; wv + 1 < wave_lo.size(); ++wv) {
-        const uint64_t d0 = wave_lo[wv], d1 = wave_lo[wv + 1];
-        const uint64_t slots = tab_off[d1 - 1] + tab_slots[d1 - 1];
-        COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
-        wa.seg_lo = doc_segs[d0];
-        wa.seg_hi = doc_segs[d1];
-        wa.r_lo = seg_rbase[wa.seg_lo];
-        wa.r_hi = seg_rbase[wa.seg_hi];
-        if (wa.r_hi > wa.r_lo) {
-            const uint64_t runs = wa.r_hi - wa.r_lo;
-            const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (runs + kChunkRuns - 1) / kChunkRuns));
-            ck<<<grid, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
-                                     d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
-            COBS_CUDA(cudaGetLastError());
-        }
-    }
-    COBS_CUDA(cudaEventRecord(e1, st));
-    COBS_CUDA(cudaStreamSynchronize(st));
-    float ms_count = 0;
-    cudaEventElapsedTime(&ms_count, e0, e1);
-    g_timing.ms_count = ms_count;
     std::vector<uint64_t> tc(n_docs);
-    COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
-    d_tab = DevBuf();
+    if (terms_input) { // TermSet::term_count() = terms.size() (termizer.hpp:25)
+        for (uint64_t d = 0; d < n_docs; ++d) tc[d] = doc_segs[d + 1] - doc_segs[d];
+    } else {
+        std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
+        uint64_t load_div = 4; // slots >= load_div/2 * windows (load <= 2/load_div)
+        if (const char* e = std::getenv("COBS_COUNT_LOAD_DIV")) load_div = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
+        for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] * load_div / 2 + 1);
+        size_t free_b = 0, total_b = 0;
+        COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        uint64_t wave_bytes = 192ull << 20;
+        if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
+        const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
+        std::vector<uint64_t> wave_lo{0};
+        uint64_t max_slots = 0;
+        for (uint64_t d0 = 0; d0 < n_docs;) {
+            uint64_t d1 = d0, slots = 0;
+            while (d1 < n_docs && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
+                tab_off[d1] = slots; // relative to the wave's tables
+                slots += tab_slots[d1];
+                ++d1;
+            }
+            max_slots = std::max(max_slots, slots);
+            wave_lo.push_back(d1);
+            d0 = d1;
+        }
+        d_taboff.reserve(8 * n_docs);
+        d_tabslots.reserve(8 * n_docs);
+        d_tab.reserve(8 * max_slots);
+        COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_taboff.ptr, tab_off.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaEventRecord(e0, st));
+        auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
+        for (size_t wv = 0; wv + 1 < wave_lo.size(); ++wv) {
+            const uint64_t d0 = wave_lo[wv], d1 = wave_lo[wv + 1];
+            const uint64_t slots = tab_off[d1 - 1] + tab_slots[d1 - 1];
+            COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
+            wa.seg_lo = doc_segs[d0];
+            wa.seg_hi = doc_segs[d1];
+            wa.r_lo = seg_rbase[wa.seg_lo];
+            wa.r_hi = seg_rbase[wa.seg_hi];
+            if (wa.r_hi > wa.r_lo) {
+                const uint64_t runs = wa.r_hi - wa.r_lo;
+                const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (runs + kChunkRuns - 1) / kChunkRuns));
+                ck<<<grid, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
+                                         d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
+                COBS_CUDA(cudaGetLastError());
+            }
+        }
+        COBS_CUDA(cudaEventRecord(e1, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        float ms_count = 0;
+        cudaEventElapsedTime(&ms_count, e0, e1);
+        g_timing.ms_count = ms_count;
+        COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
+        d_tab = DevBuf();
+    }
 
     // ---- host: order, blocks, widths ------------------------------------
     IndexMeta meta;
@@ -535,7 +561,7 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
                                  const uint64_t* doc_segs, const std::vector<std::string>& names,
                                  const Params& P, uint8_t kind, uint64_t forced_w, int device) {
     auto t0 = std::chrono::steady_clock::now();
-    auto ix = build_device_index(seqs, seg_off, n_segs, doc_segs, names, P, kind, forced_w, device, false);
+    auto ix = build_device_index(seqs, seg_off, n_segs, doc_segs, names, P, kind, forced_w, device, false, false);
     auto t_d2h = std::chrono::steady_clock::now();
     std::vector<uint8_t> image = index_image(*ix);
     g_timing.ms_d2h = ms_since(t_d2h);

@@ -22,13 +22,14 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
                                  const Params& params, uint8_t kind, uint64_t forced_w, int device);
 // The same build, leaving the index resident in HBM (pitched, ready to
 // query); `seqs` may be a device pointer (seqs_on_device).  seg_off and
-// doc_segs are host arrays.
+// doc_segs are host arrays.  terms_input: every segment is one pre-extracted
+// term (a TermSet entry), hashed as given.
 struct DeviceIndex;
 std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint64_t* seg_off,
                                                 uint64_t n_segs, const uint64_t* doc_segs,
                                                 const std::vector<std::string>& names, const Params& P,
                                                 uint8_t kind, uint64_t forced_w, int device,
-                                                bool seqs_on_device);
+                                                bool seqs_on_device, bool terms_input = false);
 // File image (header + un-pitched payload) of a device-resident index.
 std::vector<uint8_t> index_image(const DeviceIndex& ix);
 void write_image(const std::vector<uint8_t>& image, const std::string& path);

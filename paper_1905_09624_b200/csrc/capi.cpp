@@ -309,7 +309,7 @@ int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t
         for (uint64_t d = 0; d < n_docs; ++d) nm[d] = names[d];
         auto ix = cobsg::build_device_index(seqs, seg_offsets, n_segs, doc_segs, nm, to_params(params),
                                             static_cast<uint8_t>(kind), forced_w, device,
-                                            (flags & COBS_B_DEVICE_INPUT) != 0);
+                                            (flags & COBS_B_DEVICE_INPUT) != 0, (flags & COBS_B_TERMS) != 0);
         if (out_path || image) {
             std::vector<uint8_t> img = cobsg::index_image(*ix);
             if (out_path) cobsg::write_image(img, out_path);

@@ -372,3 +372,52 @@ def test_threshold_pruning_same_hits(gpu):
     assert np.array_equal(a.hit_n, b.hit_n) and np.array_equal(a.docs, b.docs)
     assert np.array_equal(a.scores, b.scores)
     view.close()
+
+
+def test_build_from_termsets(gpu, tmp_path):
+    """build_classic / build_compact over TermSets given directly (the
+    reference's own input type): terms hashed as given -- including
+    duplicates, unsorted order and non-canonical or non-ACGT terms under
+    canonical params -- and term_count = len(terms); files byte-identical to
+    the reference's; the reference's term-length error, first failing
+    document in its order."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = random.Random(77)
+    for q, k, canonical in ((31, 1, False), (31, 3, True), (12, 2, False), (5, 1, True)):
+        docs = [(b"d%03d" % i, [rand(rng, rng.randrange(0, 400))]) for i in range(150)]
+        ts = []
+        for name, content in docs:
+            terms, _, _ = O.ref_extract_terms(content, q, canonical)
+            ts.append((name, terms))
+        # user-made TermSets: duplicates, shuffled, odd bytes, non-canonical
+        odd = [rand(rng, q, b"ACGTN") for _ in range(30)] + [rand(rng, q, b"acgt") for _ in range(5)]
+        ts.append((b"odd", odd + odd[:7]))
+        ts.append((b"empty", []))
+        shuffled = list(ts[3][1])
+        rng.shuffle(shuffled)
+        ts.append((b"shuf", shuffled + shuffled[:3]))
+        params = cb.IndexParams(q=q, k=k, canonical=canonical, block_size=32)
+        for kind in (cb.KIND_CLASSIC, cb.KIND_COMPACT):
+            path = str(tmp_path / f"t{q}{k}{kind}.cobs")
+            O.ref_build_terms_write(ts, path, q=q, k=k, canonical=canonical, block_size=32, kind=kind)
+            got = cb.build_from_terms(ts, params, kind, device=gpu)
+            assert got == open(path, "rb").read(), (q, k, canonical, kind)
+    # term length != q: classic reports the first bad document in input
+    # order (before the name check); compact in (term_count, name) order
+    # after the name check
+    bad = [(b"z", [b"A" * 31, b"C" * 30]), (b"a", [b"G" * 31] * 3 + [b"T" * 32]), (b"m", [b"A" * 31])]
+    for kind in (cb.KIND_CLASSIC, cb.KIND_COMPACT):
+        with pytest.raises(O.OracleError) as want:
+            O.ref_build_terms_write(bad, str(tmp_path / "bad.cobs"), kind=kind)
+        with pytest.raises(ValueError) as got:
+            cb.build_from_terms(bad, cb.IndexParams(), kind, device=gpu)
+        assert want.value.code == 1
+        assert str(got.value) == want.value.msg, kind
+    dup = bad + [(b"z", [b"A" * 31])]
+    for kind in (cb.KIND_CLASSIC, cb.KIND_COMPACT):
+        with pytest.raises(O.OracleError) as want:
+            O.ref_build_terms_write(dup, str(tmp_path / "dup.cobs"), kind=kind)
+        with pytest.raises((ValueError, cb.DataError)) as got:
+            cb.build_from_terms(dup, cb.IndexParams(), kind, device=gpu)
+        assert str(got.value) == want.value.msg, kind
