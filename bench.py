@@ -372,6 +372,14 @@ def run_gpu(args):
                 "termize_ms": statistics.mean(o.ms_termize for o in outs),
                 "order_ms": statistics.mean(o.ms_order for o in outs)}
 
+    lens = np.diff(qo.astype(np.int64))
+    windows = int(np.maximum(lens - cfg.q + 1, 0).sum())
+    termize_ms = statistics.mean(o.ms_termize for o in outs)
+    kmer = {"kernel": "termize_hash_kernel", "ms": termize_ms, "windows": windows,
+            "windows_per_s": windows / (termize_ms / 1e3),
+            "hashes_per_s": cfg.k * grams / (termize_ms / 1e3),
+            "bound": "integer ALU (XXH64: 19 64-bit multiplies per q=31 window)"}
+
     index_bytes = view.device_bytes()
     cpu_base = None
     build = None
@@ -416,6 +424,9 @@ def run_gpu(args):
                        "hits_identical": bool(np.array_equal(outs_pruned[-1].docs, outs_e2e[-1].docs)
                                               and np.array_equal(outs_pruned[-1].hit_n, outs_e2e[-1].hit_n))},
             "roofline": roofline,
+            # kernel 1 (q-gram extraction + canonical + XXH64 + dedup):
+            # sustained window and hash throughput, event-timed per launch
+            "kmer_kernel": kmer,
             "cpu_baseline": cpu_base,
             "build": build,
             "clocks": clk,

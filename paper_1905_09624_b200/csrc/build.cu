@@ -23,6 +23,8 @@
 #include <fstream>
 #include <numeric>
 
+#include <cub/cub.cuh>
+
 #include "build.hpp"
 #include "dev.cuh"
 #include "index.hpp"
@@ -87,6 +89,42 @@ __device__ __forceinline__ void roll_windows(const uint8_t* sb, uint64_t j0, uin
     }
 }
 
+// roll_windows over a long range with 16-byte loads: the segment bytes
+// [j0, j1 + q - 1) are pushed in order (aligned uint4 loads for the body,
+// bytes at the ragged ends), f(j, dna, code) after every complete window j
+// in [j0, j1).  Only for q <= 32.
+template <int QC, int UNROLL = 4, typename F>
+__device__ __forceinline__ void roll_range(const uint8_t* sb, uint64_t j0, uint64_t j1, uint32_t q_rt,
+                                           bool canonical, F&& f) {
+    const uint32_t q = QC ? QC : q_rt;
+    if (j1 <= j0) return;
+    Roller R(q);
+    const uint64_t end = j1 + q - 1, first = j0 + q - 1;
+    uint64_t i = j0;
+    auto push = [&](uint32_t c) {
+        R.push(c);
+        if (i >= first) f(i - (q - 1), R.dna(), canonical ? R.canon() : R.fwd);
+        ++i;
+    };
+    while (i < end && (reinterpret_cast<uintptr_t>(sb + i) & 15u)) push(__ldg(sb + i));
+    if (i + 16 <= end) { // the next 16 bytes are loaded while these are rolled
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(sb + i));
+        for (;;) {
+            const bool more = i + 32 <= end;
+            uint4 nx = v;
+            if (more) nx = __ldg(reinterpret_cast<const uint4*>(sb + i + 16));
+            const uint64_t lo = v.x | static_cast<uint64_t>(v.y) << 32, hi = v.z | static_cast<uint64_t>(v.w) << 32;
+            // (a bounded unroll: the callback may be large, and 16 inlined
+            // copies of it overflow the instruction cache)
+#pragma unroll UNROLL
+            for (int k = 0; k < 16; ++k) push(static_cast<uint32_t>((k < 8 ? lo >> (8 * k) : hi >> (8 * (k - 8))) & 0xffu));
+            if (!more) break;
+            v = nx;
+        }
+    }
+    while (i < end) push(__ldg(sb + i));
+}
+
 template <int QC>
 __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long long* tab,
                                                     const uint64_t* tab_off, const uint64_t* tab_slots,
@@ -143,6 +181,255 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
     }
 }
 
+// ---- partitioned distinct count (q <= 32: every counted window is a 2-bit
+// code).  Instead of one random L2/DRAM CAS per window into a per-document
+// hash set, each document's codes are split by the top bits of a bijective
+// mix into buckets of <= ~4,096 keys (chunk histograms in shared memory, one
+// global atomic per (chunk, bucket)), scattered into a key buffer, and every
+// bucket is deduplicated by one CTA in a shared-memory set.  Exact: a code
+// lands in exactly one bucket, and equal codes always in the same one.
+constexpr uint32_t kPcRunsPerThread = 16; // consecutive runs one thread rolls through
+constexpr uint32_t kPcRuns = 256 * kPcRunsPerThread; // runs (x kBRun windows) per chunk
+constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in shared memory
+constexpr uint32_t kPcMaxSlots = 16384; // largest dedup set (128 KB of shared memory)
+constexpr uint64_t kPcTarget = 2048;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
+
+struct PcDoc {
+    uint64_t run_lo, run_hi; // global run range of the document
+    uint64_t seg_lo, seg_hi; // its segments
+    uint64_t chunk0;         // first chunk (wave-relative prefix)
+    uint64_t bucket0;        // first bucket (wave-relative prefix)
+    uint32_t nbk;            // buckets (a power of two)
+    uint32_t shift;          // 64 - log2(nbk); 64 = a single bucket
+    uint32_t doc;            // global document index
+    uint32_t pad;
+};
+
+struct PcArgs {
+    WinArgs a;
+    const PcDoc* docs;
+    uint32_t ndocs;
+    uint64_t nchunks;
+    uint32_t* bucket_cnt;     // per bucket (histogram pass)
+    uint32_t* cursor;         // per bucket write cursor (= exclusive scan of bucket_cnt)
+    unsigned long long* keys; // code + 1, grouped by bucket
+    unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
+};
+
+__device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
+    return shift >= 64 ? 0u : static_cast<uint32_t>(mix_code(code) >> shift);
+}
+
+// chunk c -> its document (last i with docs[i].chunk0 <= c, skipping empty ones)
+__device__ __forceinline__ uint32_t pc_chunk_doc(const PcDoc* docs, uint32_t n, uint64_t c) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (docs[mid].chunk0 <= c)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// f(dna, code) for every window of the chunk's runs; each thread rolls
+// through kPcRunsPerThread consecutive runs (256 threads per CTA)
+template <int QC, typename F>
+__device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uint64_t r0, uint64_t r1, F&& f) {
+    const uint32_t q = QC ? QC : a.q;
+    uint64_t g = r0 + static_cast<uint64_t>(threadIdx.x) * kPcRunsPerThread;
+    const uint64_t ge = min(r1, g + kPcRunsPerThread);
+    while (g < ge) {
+        const uint64_t s = find_seg_in(a, g, D.seg_lo, D.seg_hi);
+        const uint64_t rb = a.seg_rbase[s];
+        const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
+        const uint64_t W = len >= q ? len - q + 1 : 0;
+        const uint64_t gend = min(ge, a.seg_rbase[s + 1]);
+        roll_range<QC>(a.seqs + a.seg_off[s], (g - rb) * kBRun, min(W, (gend - rb) * kBRun), q, a.canonical != 0,
+                       [&](uint64_t, bool dna, uint64_t code) { f(dna, code); });
+        g = gend;
+    }
+}
+
+template <int QC>
+__global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
+    __shared__ uint32_t s_hist[kPcHist];
+    __shared__ uint32_t s_doc;
+    __shared__ unsigned long long s_bad;
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
+            s_bad = 0;
+        }
+        __syncthreads();
+        const PcDoc D = p.docs[s_doc];
+        const bool local = D.nbk <= kPcHist;
+        if (local)
+            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_hist[j] = 0;
+        __syncthreads();
+        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        uint32_t bad = 0;
+        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            if (!dna) { // canonical: skipped (termizer.cpp:113-116); else needs the byte path
+                bad += p.a.canonical ? 0u : 1u;
+                return;
+            }
+            const uint32_t b = pc_bucket(code, D.shift);
+            if (local)
+                atomicAdd(&s_hist[b], 1u);
+            else
+                atomicAdd(&p.bucket_cnt[D.bucket0 + b], 1u);
+        });
+        if (bad) atomicAdd(&s_bad, (unsigned long long)bad);
+        __syncthreads();
+        if (local)
+            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x)
+                if (s_hist[j]) atomicAdd(&p.bucket_cnt[D.bucket0 + j], s_hist[j]);
+        if (threadIdx.x == 0 && s_bad) atomicAdd(p.bad, s_bad);
+    }
+}
+
+template <int QC>
+__global__ void __launch_bounds__(256) pc_scatter_kernel(PcArgs p) {
+    extern __shared__ uint32_t pc_smem[];
+    uint32_t* s_cnt = pc_smem;            // kPcHist
+    uint32_t* s_base = pc_smem + kPcHist; // kPcHist
+    __shared__ uint32_t s_doc;
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
+        __syncthreads();
+        const PcDoc D = p.docs[s_doc];
+        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        if (D.nbk > kPcHist) { // very large document: one global cursor atomic per key
+            pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+                if (!dna) return;
+                const uint32_t pos = atomicAdd(&p.cursor[D.bucket0 + pc_bucket(code, D.shift)], 1u);
+                p.keys[pos] = code + 1ull;
+            });
+            continue;
+        }
+        for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_cnt[j] = 0;
+        __syncthreads();
+        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            if (dna) atomicAdd(&s_cnt[pc_bucket(code, D.shift)], 1u);
+        });
+        __syncthreads();
+        for (uint32_t j0 = threadIdx.x; j0 < D.nbk; j0 += 4 * blockDim.x) { // 4 reservations in flight
+            uint32_t n[4], base[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * blockDim.x;
+                n[u] = j < D.nbk ? s_cnt[j] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (n[u]) base[u] = atomicAdd(&p.cursor[D.bucket0 + j0 + u * blockDim.x], n[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * blockDim.x;
+                if (n[u]) s_base[j] = base[u];
+                if (j < D.nbk) s_cnt[j] = 0;
+            }
+        }
+        __syncthreads();
+        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            if (!dna) return;
+            const uint32_t b = pc_bucket(code, D.shift);
+            p.keys[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = code + 1ull;
+        });
+    }
+}
+
+// any byte outside {A,C,G,T} in [0, n)?  (without canonicalisation such
+// windows need the byte path, which the partitioned count does not have)
+__global__ void any_non_acgt_kernel(const uint8_t* p, uint64_t n, unsigned int* found) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t bad = 0;
+    const uint64_t align = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+    const uint64_t head = n < align ? n : align;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < head; i += stride) bad |= !acgt_bit(p[i]);
+    const uint4* v = reinterpret_cast<const uint4*>(p + head);
+    const uint64_t nv = (n - head) / 16;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 x = __ldcs(v + i);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) bad |= !acgt_bit((w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    }
+    for (uint64_t i = head + nv * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        bad |= !acgt_bit(p[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(found, 1u);
+}
+
+// bucket -> document of a wave
+__global__ void pc_bdoc_kernel(const PcDoc* docs, uint32_t ndocs, uint32_t* bucket_doc) {
+    for (uint32_t i = blockIdx.x; i < ndocs; i += gridDim.x) {
+        const PcDoc D = docs[i];
+        for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) bucket_doc[D.bucket0 + j] = D.doc;
+    }
+}
+
+// one CTA per bucket: distinct keys through a shared-memory set sized to the
+// bucket; the count goes to the bucket's document
+__global__ void __launch_bounds__(256) pc_dedup_kernel(const uint32_t* off, uint64_t nbuckets,
+                                                       const unsigned long long* keys, const uint32_t* bucket_doc,
+                                                       unsigned long long* term_count, unsigned int* overflow,
+                                                       uint32_t slots) {
+    extern __shared__ unsigned long long s_tab[]; // `slots` (sized per wave: 2x its largest mean bucket)
+    for (uint64_t t = blockIdx.x; t < nbuckets; t += gridDim.x) {
+        const uint32_t o0 = off[t], o1 = off[t + 1];
+        if (o0 == o1) continue; // uniform over the CTA
+        uint32_t S = 64, S_log2 = 6;
+        while (S < 2 * (o1 - o0) && S < slots) {
+            S <<= 1;
+            ++S_log2;
+        }
+        __syncthreads(); // the previous bucket's inserts are done
+        for (uint32_t j = threadIdx.x; j < S; j += blockDim.x) s_tab[j] = 0ull;
+        __syncthreads();
+        uint32_t mine = 0;
+        bool stuck = false;
+        auto insert = [&](unsigned long long key) {
+            // keys of a bucket are codes spread by the bucket's mix, so a
+            // 32-bit multiplicative hash suffices for the slot
+            uint32_t slot = ((static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * 0x9E3779B1u) >> (32 - S_log2);
+            for (uint32_t probes = 0;; slot = (slot + 1) & (S - 1)) {
+                if (++probes > S) {
+                    stuck = true;
+                    return;
+                }
+                unsigned long long cur = s_tab[slot];
+                if (cur == 0ull) {
+                    cur = atomicCAS(&s_tab[slot], 0ull, key);
+                    if (cur == 0ull) {
+                        ++mine;
+                        return;
+                    }
+                }
+                if (cur == key) return;
+            }
+        };
+        // 8 independent key loads in flight per thread, then the inserts
+        for (uint32_t i0 = o0 + threadIdx.x; i0 < o1; i0 += 8 * blockDim.x) {
+            unsigned long long kv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                kv[u] = i < o1 ? __ldcs(keys + i) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (kv[u]) insert(kv[u]);
+        }
+        mine = __reduce_add_sync(0xffffffffu, mine);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&term_count[bucket_doc[t]], (unsigned long long)mine);
+        if (stuck) atomicOr(overflow, 1u);
+    }
+}
+
 // ---- slab fill: the bits of 32 consecutive columns of a block are one u32
 // per row -- a dense "slab" of w words.  A wave of such slabs (sized to stay
 // L2-resident) is filled with atomicOr, then copied into the matrix's 4-byte
@@ -150,22 +437,35 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
 // read-modify-writes straight into the whole (HBM-sized) matrix.
 
 struct SlabDoc {
-    uint64_t run_lo, seg_lo, seg_hi; // first run and segment range of the document
+    uint64_t run_lo, run_hi, seg_lo, seg_hi; // run and segment ranges of the document
     uint64_t slab;                   // u32 index of its slab's row 0 in the wave buffer
     uint64_t w, magic;
     uint32_t bit;                    // column % 32
 };
-struct SlabGroup {
-    uint64_t src;   // u32 index of row 0 in the wave buffer
-    uint64_t dst;   // payload byte offset of (row 0, byte 4 * group)
+// A run of <= kUnitGroups consecutive 32-column groups of one block, their
+// slabs consecutive (group-major) in the stage buffer: copied into the
+// payload row by row, 4 * ng contiguous bytes per row (whole 32-byte sectors
+// when ng = 8, so DRAM sees no partial-sector writes).
+struct CopyUnit {
+    uint64_t src; // u32 index of the first group's row 0 in the stage
+    uint64_t dst; // payload byte offset of (row 0, first group)
     uint64_t w;
-    uint32_t pitch;
+    uint32_t ng, pitch;
 };
+constexpr uint32_t kUnitGroups = 8;
 
+// Consecutive runs one fill thread rolls through: 16 when the windows are
+// 2-bit codes (one roller warm-up per 128 windows), 1 when they may need the
+// byte path (the window bytes are re-read, and neighbouring lanes should then
+// read neighbouring bytes).
+constexpr uint32_t kFillRunsDna = 16;
+
+// every window of a document -> k bits of its slab column; one thread per
+// `rpt` consecutive runs of one document (run_prefix counts those spans)
 template <int QC>
 __global__ void __launch_bounds__(256) slab_fill_kernel(WinArgs a, const SlabDoc* docs,
                                                         const uint64_t* run_prefix, uint32_t ndocs,
-                                                        unsigned int* slab) {
+                                                        unsigned int* slab, uint32_t rpt) {
     const uint32_t q = QC ? QC : a.q;
     const uint64_t total = run_prefix[ndocs];
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
@@ -179,49 +479,61 @@ __global__ void __launch_bounds__(256) slab_fill_kernel(WinArgs a, const SlabDoc
                 hi = mid;
         }
         const SlabDoc D = docs[lo];
-        const uint64_t g = D.run_lo + (t - run_prefix[lo]);
-        const uint64_t s = find_seg_in(a, g, D.seg_lo, D.seg_hi);
-        const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
-        const uint64_t W = len >= q ? len - q + 1 : 0;
-        const uint64_t j0 = (g - a.seg_rbase[s]) * kBRun;
-        const uint64_t j1 = min(W, j0 + kBRun);
-        const uint8_t* sb = a.seqs + a.seg_off[s];
         unsigned int* col = slab + D.slab;
         const unsigned int bit = 1u << D.bit;
-        roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
-            const uint8_t* w = sb + j;
-            if (dna) {
-                for (uint32_t seed = 0; seed < a.k; ++seed)
-                    atomicOr(col + fastmod(xxh64_code<QC>(code, q, seed), D.w, D.magic), bit);
-            } else if (a.canonical) {
-                if (q <= 32 || !window_acgt(w, q)) return;
-                const bool rc = choose_rc(w, q);
-                for (uint32_t seed = 0; seed < a.k; ++seed)
-                    atomicOr(col + fastmod(xxh64_term(w, q, rc, seed), D.w, D.magic), bit);
-            } else {
-                for (uint32_t seed = 0; seed < a.k; ++seed)
-                    atomicOr(col + fastmod(xxh64_term(w, q, false, seed), D.w, D.magic), bit);
-            }
-        });
+        uint64_t g = D.run_lo + (t - run_prefix[lo]) * rpt;
+        const uint64_t ge = min(D.run_hi, g + rpt);
+        while (g < ge) {
+            const uint64_t s = find_seg_in(a, g, D.seg_lo, D.seg_hi);
+            const uint64_t rb = a.seg_rbase[s];
+            const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
+            const uint64_t W = len >= q ? len - q + 1 : 0;
+            const uint64_t gend = min(ge, a.seg_rbase[s + 1]);
+            const uint64_t j0 = (g - rb) * kBRun, j1 = min(W, (gend - rb) * kBRun);
+            const uint8_t* sb = a.seqs + a.seg_off[s];
+            auto put = [&](uint64_t j, bool dna, uint64_t code) {
+                const uint8_t* w = sb + j;
+                if (dna) {
+                    for (uint32_t seed = 0; seed < a.k; ++seed)
+                        atomicOr(col + fastmod(xxh64_code<QC>(code, q, seed), D.w, D.magic), bit);
+                } else if (a.canonical) {
+                    if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
+                    const bool rc = choose_rc(w, q);
+                    for (uint32_t seed = 0; seed < a.k; ++seed)
+                        atomicOr(col + fastmod(xxh64_term(w, q, rc, seed), D.w, D.magic), bit);
+                } else {
+                    for (uint32_t seed = 0; seed < a.k; ++seed)
+                        atomicOr(col + fastmod(xxh64_term(w, q, false, seed), D.w, D.magic), bit);
+                }
+            };
+            if (rpt == 1)
+                roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, put);
+            else if (q <= 32)
+                roll_range<QC, 1>(sb, j0, j1, q, a.canonical != 0, put);
+            else
+                for (uint64_t j = j0; j < j1; ++j) put(j, false, 0ull);
+            g = gend;
+        }
     }
 }
 
-__global__ void slab_copy_kernel(const SlabGroup* groups, const uint64_t* row_prefix, uint32_t ngroups,
-                                 const unsigned int* slab, uint8_t* payload) {
-    const uint64_t total = row_prefix[ngroups];
+__global__ void unit_copy_kernel(const CopyUnit* units, const uint64_t* prefix, uint32_t nunits,
+                                 const unsigned int* stage, uint8_t* payload) {
+    const uint64_t total = prefix[nunits];
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = ngroups;
+        uint32_t lo = 0, hi = nunits;
         while (hi - lo > 1) {
             uint32_t mid = (lo + hi) >> 1;
-            if (row_prefix[mid] <= t)
+            if (prefix[mid] <= t)
                 lo = mid;
             else
                 hi = mid;
         }
-        const SlabGroup G = groups[lo];
-        const uint64_t r = t - row_prefix[lo];
-        *reinterpret_cast<unsigned int*>(payload + G.dst + r * G.pitch) = slab[G.src + r];
+        const CopyUnit U = units[lo];
+        const uint64_t local = t - prefix[lo];
+        const uint64_t r = local / U.ng, x = local - r * U.ng;
+        *reinterpret_cast<unsigned int*>(payload + U.dst + r * U.pitch + 4 * x) = stage[U.src + x * U.w + r];
     }
 }
 
@@ -314,7 +626,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     const uint64_t total_bytes = n_segs ? seg_off[n_segs] : 0;
     const uint64_t total_runs = seg_rbase[n_segs];
 
-    DevBuf d_seqs, d_segoff, d_segw, d_segdoc, d_docstart, d_tab, d_taboff, d_tabslots, d_tc;
+    DevBuf d_seqs, d_segoff, d_segw, d_segdoc, d_docstart, d_tc;
     if (!seqs_on_device) d_seqs.reserve(std::max<uint64_t>(total_bytes, 1));
     d_segoff.reserve(8 * (n_segs + 1));
     d_segw.reserve(8 * (n_segs + 1));
@@ -352,61 +664,221 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     uint64_t slab_wave_bytes = 96ull << 20;
     if (const char* e = std::getenv("COBS_SLAB_WAVE_MB")) slab_wave_bytes = std::strtoull(e, nullptr, 10) << 20;
     std::vector<uint64_t> tc(n_docs);
+    uint32_t fill_rpt = 1; // kFillRunsDna once the count has seen only 2-bit-code windows
     if (terms_input) { // TermSet::term_count() = terms.size() (termizer.hpp:25)
         for (uint64_t d = 0; d < n_docs; ++d) tc[d] = doc_segs[d + 1] - doc_segs[d];
     } else {
-        std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
-        uint64_t load_div = 4; // slots >= load_div/2 * windows (load <= 2/load_div)
-        if (const char* e = std::getenv("COBS_COUNT_LOAD_DIV")) load_div = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
-        for (uint64_t d = 0; d < n_docs; ++d) tab_slots[d] = next_pow2(doc_w[d] * load_div / 2 + 1);
         size_t free_b = 0, total_b = 0;
-        COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        uint64_t wave_bytes = 192ull << 20;
-        if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
-        const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
-        std::vector<uint64_t> wave_lo{0};
-        uint64_t max_slots = 0;
-        for (uint64_t d0 = 0; d0 < n_docs;) {
-            uint64_t d1 = d0, slots = 0;
-            while (d1 < n_docs && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
-                tab_off[d1] = slots; // relative to the wave's tables
-                slots += tab_slots[d1];
-                ++d1;
+        // exact distinct counts by hash-set insertion (any q, any bytes) for
+        // documents [d_lo, d_hi), in waves whose sets stay L2-resident
+        auto hashset_count = [&](uint64_t d_lo, uint64_t d_hi) {
+            std::vector<uint64_t> tab_off(n_docs), tab_slots(n_docs);
+            uint64_t load_div = 4; // slots >= load_div/2 * windows (load <= 2/load_div)
+            if (const char* e = std::getenv("COBS_COUNT_LOAD_DIV")) load_div = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
+            for (uint64_t d = d_lo; d < d_hi; ++d) tab_slots[d] = next_pow2(doc_w[d] * load_div / 2 + 1);
+            COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            uint64_t wave_bytes = 192ull << 20;
+            if (const char* e = std::getenv("COBS_COUNT_WAVE_MB")) wave_bytes = std::strtoull(e, nullptr, 10) << 20;
+            const uint64_t budget_slots = std::max<uint64_t>(std::min<uint64_t>((free_b / 3) / 8, wave_bytes / 8), 1ull << 16);
+            std::vector<uint64_t> wave_lo{d_lo};
+            uint64_t max_slots = 0;
+            for (uint64_t d0 = d_lo; d0 < d_hi;) {
+                uint64_t d1 = d0, slots = 0;
+                while (d1 < d_hi && (d1 == d0 || slots + tab_slots[d1] <= budget_slots)) {
+                    tab_off[d1] = slots; // relative to the wave's tables
+                    slots += tab_slots[d1];
+                    ++d1;
+                }
+                max_slots = std::max(max_slots, slots);
+                wave_lo.push_back(d1);
+                d0 = d1;
             }
-            max_slots = std::max(max_slots, slots);
-            wave_lo.push_back(d1);
-            d0 = d1;
-        }
-        d_taboff.reserve(8 * n_docs);
-        d_tabslots.reserve(8 * n_docs);
-        d_tab.reserve(8 * max_slots);
-        COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
-        COBS_CUDA(cudaMemcpyAsync(d_taboff.ptr, tab_off.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
-        COBS_CUDA(cudaEventRecord(e0, st));
-        auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
-        for (size_t wv = 0; wv + 1 < wave_lo.size(); ++wv) {
-            const uint64_t d0 = wave_lo[wv], d1 = wave_lo[wv + 1];
-            const uint64_t slots = tab_off[d1 - 1] + tab_slots[d1 - 1];
-            COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
-            wa.seg_lo = doc_segs[d0];
-            wa.seg_hi = doc_segs[d1];
-            wa.r_lo = seg_rbase[wa.seg_lo];
-            wa.r_hi = seg_rbase[wa.seg_hi];
-            if (wa.r_hi > wa.r_lo) {
-                const uint64_t runs = wa.r_hi - wa.r_lo;
-                const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (runs + kChunkRuns - 1) / kChunkRuns));
-                ck<<<grid, 256, 0, st>>>(wa, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
-                                         d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
+            DevBuf d_tab, d_taboff, d_tabslots;
+            d_taboff.reserve(8 * n_docs);
+            d_tabslots.reserve(8 * n_docs);
+            d_tab.reserve(8 * std::max<uint64_t>(max_slots, 1));
+            COBS_CUDA(cudaMemcpyAsync(d_tabslots.ptr, tab_slots.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+            COBS_CUDA(cudaMemcpyAsync(d_taboff.ptr, tab_off.data(), 8 * n_docs, cudaMemcpyHostToDevice, st));
+            // (short runs per lane on purpose: a CTA's windows stay within one
+            // or two documents, so the sets it touches stay L2-resident)
+            auto ck = q == 31 ? count_kernel<31> : count_kernel<0>;
+            const uint64_t span = kChunkRuns;
+            for (size_t wv = 0; wv + 1 < wave_lo.size(); ++wv) {
+                const uint64_t d0 = wave_lo[wv], d1 = wave_lo[wv + 1];
+                const uint64_t slots = tab_off[d1 - 1] + tab_slots[d1 - 1];
+                COBS_CUDA(cudaMemsetAsync(d_tab.ptr, 0, 8 * slots, st));
+                WinArgs w = wa;
+                w.seg_lo = doc_segs[d0];
+                w.seg_hi = doc_segs[d1];
+                w.r_lo = seg_rbase[w.seg_lo];
+                w.r_hi = seg_rbase[w.seg_hi];
+                if (w.r_hi > w.r_lo) {
+                    const uint64_t runs = w.r_hi - w.r_lo;
+                    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (runs + span - 1) / span));
+                    ck<<<grid, 256, 0, st>>>(w, d_tab.as<unsigned long long>(), d_taboff.as<uint64_t>(),
+                                             d_tabslots.as<uint64_t>(), d_tc.as<unsigned long long>());
+                    COBS_CUDA(cudaGetLastError());
+                }
+            }
+            COBS_CUDA(cudaStreamSynchronize(st)); // tables die with this scope
+        };
+
+        // partitioned count for q <= 32 (see pc_hist_kernel), in waves of
+        // documents whose windows fit the key buffer; a wave that meets a
+        // window needing the byte path (non-ACGT, no canonicalisation) or a
+        // bucket too skewed for its set is recounted by hashset_count
+        auto partitioned_count = [&] {
+            COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            uint64_t kmax = std::min<uint64_t>((free_b / 2) / 8, 0xffffffffull);
+            if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
+            kmax = std::max<uint64_t>(kmax, 1);
+            const uint64_t max_buckets = kmax / (kPcTarget / 2) + 2 * n_docs + 1;
+            // plan every wave up front (documents in order, keys <= kmax); the
+            // waves then run back to back without a host round trip
+            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys; };
+            std::vector<PcWave> pw;
+            std::vector<PcDoc> pd;
+            std::vector<std::pair<uint64_t, uint64_t>> oversize; // documents beyond the key buffer
+            for (uint64_t d0 = 0; d0 < n_docs;) {
+                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0};
+                uint64_t d1 = d0;
+                while (d1 < n_docs) {
+                    const uint64_t W = doc_w[d1];
+                    uint64_t nbk = 1;
+                    while (nbk * kPcTarget < W && nbk < kPcHist) nbk <<= 1;
+                    // the set must hold a bucket's distinct keys: mean W / nbk, plus slack
+                    const uint64_t mean = (W + nbk - 1) / nbk;
+                    uint64_t slots = 256;
+                    while (slots < 2 * mean + 8 * 64 && slots < kPcMaxSlots) slots <<= 1;
+                    if (d1 > d0 && (wv.keys + W > kmax || wv.nbuck + nbk > max_buckets)) break;
+                    wv.slots = std::max(wv.slots, slots);
+                    PcDoc D{};
+                    D.seg_lo = doc_segs[d1];
+                    D.seg_hi = doc_segs[d1 + 1];
+                    D.run_lo = seg_rbase[D.seg_lo];
+                    D.run_hi = seg_rbase[D.seg_hi];
+                    D.chunk0 = wv.nchunk;
+                    D.bucket0 = wv.nbuck;
+                    D.nbk = static_cast<uint32_t>(nbk);
+                    D.shift = 64 - static_cast<uint32_t>(__builtin_ctzll(nbk));
+                    D.doc = static_cast<uint32_t>(d1);
+                    pd.push_back(D);
+                    wv.keys += W;
+                    wv.nbuck += nbk;
+                    wv.nchunk += (D.run_hi - D.run_lo + kPcRuns - 1) / kPcRuns;
+                    ++d1;
+                }
+                wv.d1 = d1;
+                if (wv.keys > kmax || wv.nbuck > max_buckets) {
+                    pd.resize(wv.doc0);
+                    oversize.push_back({d0, d1});
+                } else {
+                    pw.push_back(wv);
+                }
+                d0 = d1;
+            }
+            uint64_t max_keys = 1, max_nbuck = 1;
+            for (const PcWave& wv : pw) {
+                max_keys = std::max(max_keys, wv.keys);
+                max_nbuck = std::max(max_nbuck, wv.nbuck);
+            }
+            DevBuf d_keys, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc;
+            d_keys.reserve(8 * max_keys);
+            d_flags.reserve(16 * std::max<size_t>(pw.size(), 1));
+            d_cnt.reserve(4 * (max_nbuck + 1));
+            d_off.reserve(4 * (max_nbuck + 1));
+            d_bdoc.reserve(4 * (max_nbuck + 1));
+            d_docs.reserve(sizeof(PcDoc) * std::max<size_t>(pd.size(), 1));
+            size_t tmp_bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt.as<uint32_t>(), d_off.as<uint32_t>(),
+                                          static_cast<int>(max_nbuck + 1), st);
+            d_tmp.reserve(std::max<size_t>(tmp_bytes, 16));
+            if (!pd.empty())
+                COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
+            COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
+            auto hist = q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
+            auto scat = q == 31 ? pc_scatter_kernel<31> : pc_scatter_kernel<0>;
+            COBS_CUDA(cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
+            COBS_CUDA(cudaFuncSetAttribute(pc_dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
+            for (size_t i = 0; i < pw.size(); ++i) {
+                const PcWave& wv = pw[i];
+                const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
+                unsigned long long* flags = d_flags.as<unsigned long long>() + 2 * i;
+                COBS_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 4 * (wv.nbuck + 1), st));
+                pc_bdoc_kernel<<<std::min<uint32_t>(nd, 148 * 8), 256, 0, st>>>(d_docs.as<PcDoc>() + wv.doc0, nd,
+                                                                               d_bdoc.as<uint32_t>());
+                PcArgs pa{};
+                pa.a = wa;
+                pa.docs = d_docs.as<PcDoc>() + wv.doc0;
+                pa.ndocs = nd;
+                pa.nchunks = wv.nchunk;
+                pa.bucket_cnt = d_cnt.as<uint32_t>();
+                pa.keys = d_keys.as<unsigned long long>();
+                pa.bad = flags;
+                const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
+                if (wv.nchunk) hist<<<grid, 256, 0, st>>>(pa);
+                size_t tb = d_tmp.bytes;
+                COBS_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.ptr, tb, d_cnt.as<uint32_t>(), d_off.as<uint32_t>(),
+                                                        static_cast<int>(wv.nbuck + 1), st));
+                // the scan is both the dedup's bucket offsets and (a copy) the scatter cursors
+                COBS_CUDA(cudaMemcpyAsync(d_cnt.ptr, d_off.ptr, 4 * (wv.nbuck + 1), cudaMemcpyDeviceToDevice, st));
+                pa.cursor = d_cnt.as<uint32_t>();
+                if (wv.nchunk) {
+                    scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
+                    pc_dedup_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), 256, wv.slots * 8, st>>>(
+                        d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
+                        d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
+                        static_cast<uint32_t>(wv.slots));
+                }
                 COBS_CUDA(cudaGetLastError());
             }
+            g_timing.count_waves = static_cast<uint32_t>(pw.size());
+            std::vector<uint64_t> flags(2 * pw.size());
+            if (!pw.empty())
+                COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 16 * pw.size(), cudaMemcpyDeviceToHost, st));
+            COBS_CUDA(cudaStreamSynchronize(st));
+            d_keys.release(); // before any recount needs the memory
+            bool byte_windows = !oversize.empty();
+            for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
+            if (!byte_windows) fill_rpt = kFillRunsDna;
+            for (size_t i = 0; i < pw.size(); ++i)
+                if (flags[2 * i] || (flags[2 * i + 1] & 0xffffffffull)) { // recount this wave exactly
+                    COBS_CUDA(cudaMemsetAsync(d_tc.as<unsigned long long>() + pw[i].d0, 0, 8 * (pw[i].d1 - pw[i].d0), st));
+                    hashset_count(pw[i].d0, pw[i].d1);
+                    ++g_timing.count_fallback_waves;
+                }
+            for (const auto& r : oversize) hashset_count(r.first, r.second);
+        };
+
+        COBS_CUDA(cudaEventRecord(e0, st));
+        const char* pc_env = std::getenv("COBS_COUNT_PARTITION");
+        // (small corpora: the hash sets are L2-resident anyway and need no
+        // key buffer; COBS_COUNT_PARTITION=1 forces the partitioned count)
+        uint64_t total_w = 0;
+        for (uint64_t d = 0; d < n_docs; ++d) total_w += doc_w[d];
+        bool use_pc = q <= 32 && (pc_env ? pc_env[0] == '1' : total_w >= (1ull << 30));
+        const char* scan_env = std::getenv("COBS_PC_NO_SCAN"); // tests: reach the per-wave fallback
+        if (use_pc && !wa.canonical && total_bytes && !(scan_env && scan_env[0] == '1')) {
+            // byte-path windows ahead? then the hash sets straight away
+            DevBuf d_found;
+            d_found.reserve(4);
+            COBS_CUDA(cudaMemsetAsync(d_found.ptr, 0, 4, st));
+            any_non_acgt_kernel<<<148 * 8, 256, 0, st>>>(wa.seqs, total_bytes, d_found.as<unsigned int>());
+            uint32_t found = 0;
+            COBS_CUDA(cudaMemcpyAsync(&found, d_found.ptr, 4, cudaMemcpyDeviceToHost, st));
+            COBS_CUDA(cudaStreamSynchronize(st));
+            use_pc = found == 0;
         }
+        if (use_pc)
+            partitioned_count();
+        else
+            hashset_count(0, n_docs);
         COBS_CUDA(cudaEventRecord(e1, st));
         COBS_CUDA(cudaStreamSynchronize(st));
         float ms_count = 0;
         cudaEventElapsedTime(&ms_count, e0, e1);
         g_timing.ms_count = ms_count;
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
-        d_tab = DevBuf();
     }
 
     // ---- host: order, blocks, widths ------------------------------------
@@ -450,78 +922,107 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     wa.seg_lo = 0;
     wa.seg_hi = n_segs;
     if (total_runs > 0) {
-        // waves of whole 32-column groups, block-major, slabs <= wave_bytes
+        // Stage batches of whole copy units (<= 8 consecutive groups of one
+        // block, slabs group-major); inside a batch, fill waves of whole
+        // groups whose slabs stay L2-resident (<= slab_wave_bytes); after a
+        // batch's waves, one unit_copy launch moves it into the payload.
         std::vector<SlabDoc> sdocs;
-        std::vector<uint64_t> run_prefix;   // per wave: ndocs+1 entries (concatenated)
-        std::vector<SlabGroup> sgroups;
-        std::vector<uint64_t> row_prefix;   // per wave: ngroups+1 entries (concatenated)
-        struct Wave { size_t doc0, ndocs, rp0, grp0, ngroups, gp0; uint64_t words; };
+        std::vector<uint64_t> run_prefix; // per fill wave: ndocs+1 entries (concatenated)
+        std::vector<CopyUnit> units;
+        std::vector<uint64_t> unit_prefix; // per batch: nunits+1 entries (concatenated)
+        struct Wave { size_t doc0, ndocs, rp0; uint64_t w_lo, w_hi; };
+        struct Batch { size_t wave0, nwaves, unit0, nunits, up0; };
         std::vector<Wave> waves;
-        Wave cur{0, 0, 0, 0, 0, 0, 0};
-        uint64_t max_words = 0;
-        auto close_wave = [&] {
-            if (cur.ngroups == 0) return;
-            max_words = std::max(max_words, cur.words);
-            waves.push_back(cur);
-            cur = Wave{sdocs.size(), 0, run_prefix.size(), sgroups.size(), 0, row_prefix.size(), 0};
-        };
+        std::vector<Batch> batches;
+        uint64_t max_w = 1;
+        for (uint64_t b = 0; b < nb; ++b) max_w = std::max<uint64_t>(max_w, ix->blocks[b].w);
         const uint64_t wave_words = std::max<uint64_t>(slab_wave_bytes / 4, 1);
+        const uint64_t stage_words = std::max<uint64_t>(kUnitGroups * max_w, std::max<uint64_t>(wave_words, 64ull << 20));
+        uint64_t words = 0, max_words = 0; // stage fill of the open batch
+        bool wave_open = false, batch_open = false;
+        auto close_wave = [&] {
+            if (!wave_open) return;
+            waves.back().w_hi = words;
+            wave_open = false;
+        };
+        auto close_batch = [&] {
+            if (!batch_open) return;
+            close_wave();
+            Batch& B = batches.back();
+            B.nwaves = waves.size() - B.wave0;
+            B.nunits = units.size() - B.unit0;
+            max_words = std::max(max_words, words);
+            words = 0;
+            batch_open = false;
+        };
         for (uint64_t b = 0; b < nb; ++b) {
             const DevBlock& d = ix->blocks[b];
             const uint64_t ngr = (d.dc + 31) / 32;
-            for (uint64_t gi = 0; gi < ngr; ++gi) {
-                if (cur.ngroups > 0 && cur.words + d.w > wave_words) close_wave();
-                if (cur.ngroups == 0) { // open: prefix starts
-                    cur.rp0 = run_prefix.size();
-                    cur.gp0 = row_prefix.size();
-                    run_prefix.push_back(0);
-                    row_prefix.push_back(0);
+            for (uint64_t g0 = 0; g0 < ngr; g0 += kUnitGroups) {
+                const uint32_t ng = static_cast<uint32_t>(std::min<uint64_t>(kUnitGroups, ngr - g0));
+                if (batch_open && words + ng * d.w > stage_words) close_batch();
+                if (!batch_open) {
+                    batches.push_back(Batch{waves.size(), 0, units.size(), 0, unit_prefix.size()});
+                    unit_prefix.push_back(0);
+                    batch_open = true;
                 }
-                SlabGroup G{cur.words, d.base + 4 * gi, d.w, d.pitch};
-                sgroups.push_back(G);
-                row_prefix.push_back(row_prefix.back() + d.w);
-                for (uint64_t c = 32 * gi; c < std::min<uint64_t>(d.dc, 32 * gi + 32); ++c) {
-                    const uint64_t doc = order[d.doc_base + c];
-                    SlabDoc D{};
-                    D.seg_lo = doc_segs[doc];
-                    D.seg_hi = doc_segs[doc + 1];
-                    D.run_lo = seg_rbase[D.seg_lo];
-                    D.slab = cur.words;
-                    D.w = d.w;
-                    D.magic = d.magic;
-                    D.bit = static_cast<uint32_t>(c % 32);
-                    sdocs.push_back(D);
-                    run_prefix.push_back(run_prefix.back() + (seg_rbase[D.seg_hi] - D.run_lo));
-                    ++cur.ndocs;
+                units.push_back(CopyUnit{words, d.base + 4 * g0, d.w, ng, d.pitch});
+                unit_prefix.push_back(unit_prefix.back() + ng * d.w);
+                for (uint64_t gi = g0; gi < g0 + ng; ++gi) {
+                    if (wave_open && words + d.w - waves.back().w_lo > wave_words) close_wave();
+                    if (!wave_open) {
+                        waves.push_back(Wave{sdocs.size(), 0, run_prefix.size(), words, words});
+                        run_prefix.push_back(0);
+                        wave_open = true;
+                    }
+                    Wave& wv = waves.back();
+                    for (uint64_t c = 32 * gi; c < std::min<uint64_t>(d.dc, 32 * gi + 32); ++c) {
+                        const uint64_t doc = order[d.doc_base + c];
+                        SlabDoc D{};
+                        D.seg_lo = doc_segs[doc];
+                        D.seg_hi = doc_segs[doc + 1];
+                        D.run_lo = seg_rbase[D.seg_lo];
+                        D.run_hi = seg_rbase[D.seg_hi];
+                        D.slab = words;
+                        D.w = d.w;
+                        D.magic = d.magic;
+                        D.bit = static_cast<uint32_t>(c % 32);
+                        sdocs.push_back(D);
+                        run_prefix.push_back(run_prefix.back() + (D.run_hi - D.run_lo + fill_rpt - 1) / fill_rpt);
+                        ++wv.ndocs;
+                    }
+                    words += d.w;
                 }
-                cur.words += d.w;
-                ++cur.ngroups;
             }
         }
-        close_wave();
-        DevBuf d_sdocs, d_rp, d_sgroups, d_gp, d_slab;
+        close_batch();
+        DevBuf d_sdocs, d_rp, d_units, d_up, d_slab;
         d_sdocs.reserve(sizeof(SlabDoc) * std::max<size_t>(sdocs.size(), 1));
         d_rp.reserve(8 * run_prefix.size());
-        d_sgroups.reserve(sizeof(SlabGroup) * std::max<size_t>(sgroups.size(), 1));
-        d_gp.reserve(8 * row_prefix.size());
+        d_units.reserve(sizeof(CopyUnit) * std::max<size_t>(units.size(), 1));
+        d_up.reserve(8 * unit_prefix.size());
         d_slab.reserve(4 * std::max<uint64_t>(max_words, 1));
         COBS_CUDA(cudaMemcpyAsync(d_sdocs.ptr, sdocs.data(), sizeof(SlabDoc) * sdocs.size(), cudaMemcpyHostToDevice, st));
         COBS_CUDA(cudaMemcpyAsync(d_rp.ptr, run_prefix.data(), 8 * run_prefix.size(), cudaMemcpyHostToDevice, st));
-        COBS_CUDA(cudaMemcpyAsync(d_sgroups.ptr, sgroups.data(), sizeof(SlabGroup) * sgroups.size(),
-                                  cudaMemcpyHostToDevice, st));
-        COBS_CUDA(cudaMemcpyAsync(d_gp.ptr, row_prefix.data(), 8 * row_prefix.size(), cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_units.ptr, units.data(), sizeof(CopyUnit) * units.size(), cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaMemcpyAsync(d_up.ptr, unit_prefix.data(), 8 * unit_prefix.size(), cudaMemcpyHostToDevice, st));
         COBS_CUDA(cudaEventRecord(e2, st));
         auto fk = q == 31 ? slab_fill_kernel<31> : slab_fill_kernel<0>;
-        for (const Wave& wv : waves) {
-            COBS_CUDA(cudaMemsetAsync(d_slab.ptr, 0, 4 * wv.words, st));
-            const uint64_t runs = run_prefix[wv.rp0 + wv.ndocs];
-            if (runs > 0)
-                fk<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (runs + 255) / 256)), 256, 0, st>>>(
-                    wa, d_sdocs.as<SlabDoc>() + wv.doc0, d_rp.as<uint64_t>() + wv.rp0,
-                    static_cast<uint32_t>(wv.ndocs), d_slab.as<unsigned int>());
-            slab_copy_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (wv.words + 255) / 256)), 256, 0,
-                               st>>>(d_sgroups.as<SlabGroup>() + wv.grp0, d_gp.as<uint64_t>() + wv.gp0,
-                                     static_cast<uint32_t>(wv.ngroups), d_slab.as<unsigned int>(), ix->payload);
+        for (const Batch& B : batches) {
+            for (size_t i = B.wave0; i < B.wave0 + B.nwaves; ++i) {
+                const Wave& wv = waves[i];
+                COBS_CUDA(cudaMemsetAsync(d_slab.as<unsigned int>() + wv.w_lo, 0, 4 * (wv.w_hi - wv.w_lo), st));
+                const uint64_t runs = run_prefix[wv.rp0 + wv.ndocs];
+                if (runs > 0)
+                    fk<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (runs + 255) / 256)), 256, 0, st>>>(
+                        wa, d_sdocs.as<SlabDoc>() + wv.doc0, d_rp.as<uint64_t>() + wv.rp0,
+                        static_cast<uint32_t>(wv.ndocs), d_slab.as<unsigned int>(), fill_rpt);
+                COBS_CUDA(cudaGetLastError());
+            }
+            const uint64_t total = unit_prefix[B.up0 + B.nunits];
+            unit_copy_kernel<<<static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 16, (total + 255) / 256))),
+                               256, 0, st>>>(d_units.as<CopyUnit>() + B.unit0, d_up.as<uint64_t>() + B.up0,
+                                             static_cast<uint32_t>(B.nunits), d_slab.as<unsigned int>(), ix->payload);
             COBS_CUDA(cudaGetLastError());
         }
         COBS_CUDA(cudaEventRecord(e3, st));

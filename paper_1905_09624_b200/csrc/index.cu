@@ -18,6 +18,11 @@ void DevBuf::reserve(size_t n) {
     COBS_CUDA(cudaMalloc(&ptr, n));
     bytes = n;
 }
+void DevBuf::release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+}
 DevBuf::~DevBuf() {
     if (ptr) cudaFree(ptr);
 }

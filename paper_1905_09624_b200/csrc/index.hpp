@@ -12,11 +12,15 @@
 
 namespace cobsg {
 
-// Grow-only device buffer.
+// Grow-only device buffer (owning, move-only).
 struct DevBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     void reserve(size_t n);
+    void release(); // free now
     template <typename T>
     T* as() const { return static_cast<T*>(ptr); }
     ~DevBuf();
@@ -25,6 +29,9 @@ struct DevBuf {
 struct PinnedBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
     void reserve(size_t n);
     template <typename T>
     T* as() const { return static_cast<T*>(ptr); }

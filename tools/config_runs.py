@@ -40,7 +40,8 @@ def column_bits(img: bytes, idx: O.OracleIndex, block: int, col: int) -> np.ndar
     return (rows[:, col // 8] >> (col % 8)) & 1
 
 
-def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0, repeat: int = 1):
+def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0, repeat: int = 1,
+        build_only: bool = False):
     cfg = synth.CONFIGS[name]
     if n_queries:
         cfg = synth.replace(cfg, n_queries=n_queries)
@@ -73,6 +74,9 @@ def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0
                     "index_bytes_hbm": view.device_bytes()}
     del dev
     torch.cuda.empty_cache()
+    if build_only:
+        view.close()
+        return res
 
     # ---- the config's query batch --------------------------------------
     qb, qo = synth.queries(cfg, lengths=lengths)
@@ -155,10 +159,11 @@ def main():
     ap.add_argument("--queries", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--build-only", action="store_true")
     a = ap.parse_args()
     results = []
     for c in a.configs:
-        r = run(c, a.docs, a.queries, a.batch, a.repeat)
+        r = run(c, a.docs, a.queries, a.batch, a.repeat, a.build_only)
         print(json.dumps(r), flush=True)
         results.append(r)
         json.dump(results, open(a.out, "w"), indent=1)
