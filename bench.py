@@ -372,6 +372,19 @@ def run_gpu(args):
                 "termize_ms": statistics.mean(o.ms_termize for o in outs),
                 "order_ms": statistics.mean(o.ms_order for o in outs)}
 
+    # same-box ceilings (after the timed region): the gather's access shape,
+    # random 128-byte lines, and a streaming read, on this GPU in this process
+    try:
+        free, _ = torch.cuda.mem_get_info(local)
+        st_gbs, rnd_gbs = cb.calibrate(local, min(16 << 30, free // 2))
+        roofline["same_box"] = {"stream_read_gbs": st_gbs, "random128_gbs": rnd_gbs,
+                                "frac_of_stream_read": achieved / st_gbs,
+                                "frac_of_random128": achieved / rnd_gbs,
+                                "what": "tools-free calibration (cobs_gpu_calibrate): random 128-byte "
+                                        "lines, 16 in flight per warp, over a 16 GiB buffer"}
+    except Exception as e:  # report, do not die
+        roofline["same_box"] = {"error": repr(e)}
+
     lens = np.diff(qo.astype(np.int64))
     windows = int(np.maximum(lens - cfg.q + 1, 0).sum())
     termize_ms = statistics.mean(o.ms_termize for o in outs)

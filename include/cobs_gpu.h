@@ -276,6 +276,12 @@ int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size,
 int cobs_gpu_synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo,
                         uint64_t doc_hi, uint8_t* dev_out, int device);
 
+/* Roofline calibration on this GPU (bench/tools; not a reference
+ * interface): HBM read GB/s for a streaming read and for random 128-byte
+ * lines in the gather kernel's access shape, over a power-of-two buffer of
+ * <= `bytes` (>= 1 GiB) allocated for the call. */
+int cobs_gpu_calibrate(int device, uint64_t bytes, double* stream_gbs, double* random128_gbs);
+
 #ifdef __cplusplus
 }
 #endif

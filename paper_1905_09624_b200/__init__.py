@@ -489,6 +489,16 @@ def build_from_terms(termsets: Sequence[Tuple[bytes, Sequence[bytes]]], params: 
         N.lib.cobs_gpu_free(img)
 
 
+def calibrate(device: int = 0, nbytes: int = 16 << 30) -> Tuple[float, float]:
+    """(streaming read GB/s, random 128-byte line GB/s) on this GPU: the
+    same-box ceiling the gather kernel is compared against in bench.py."""
+    a, b = C.c_double(), C.c_double()
+    rc = N.lib.cobs_gpu_calibrate(device, nbytes, C.byref(a), C.byref(b))
+    if rc:
+        raise CudaError("calibration failed")
+    return a.value, b.value
+
+
 def synth_docs_device(seed: int, alpha: int, lengths: np.ndarray, dev_ptr: int, device: int = 0,
                       lo: int = 0, hi: Optional[int] = None) -> None:
     """Generate seeded documents [lo, hi) straight into device memory."""

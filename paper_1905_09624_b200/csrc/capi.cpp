@@ -12,6 +12,10 @@
 #include "index.hpp"
 #include "merge.hpp"
 
+namespace cobsg {
+void calibrate(int device, uint64_t bytes, double* stream_gbs, double* random128_gbs); // calib.cu
+}
+
 struct cobs_gpu_index {
     std::unique_ptr<cobsg::DeviceIndex> ix;
 };
@@ -404,6 +408,10 @@ int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size,
 int cobs_gpu_synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo,
                         uint64_t doc_hi, uint8_t* dev_out, int device) {
     return guarded(nullptr, 0, [&] { cobsg::synth_docs(seed, alpha, doc_len, doc_lo, doc_hi, dev_out, device); });
+}
+
+int cobs_gpu_calibrate(int device, uint64_t bytes, double* stream_gbs, double* random128_gbs) {
+    return guarded(nullptr, 0, [&] { cobsg::calibrate(device, bytes, stream_gbs, random128_gbs); });
 }
 
 } // extern "C"
