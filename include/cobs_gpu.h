@@ -79,6 +79,19 @@ int cobs_gpu_index_open_image_ex(const uint8_t* image, uint64_t len, const char*
 /* 1 if the index is in the host-resident streaming mode. */
 int cobs_gpu_index_streaming(const cobs_gpu_index* index);
 
+/* Block sharding of a compact index (the reference has no
+ * sharded reader): blocks [block_lo, block_hi) of the file at `path` as a
+ * standalone compact index in HBM -- same params, those blocks and their
+ * documents, the whole header validated as by cobs_gpu_index_open.  Hit
+ * columns of a shard are local; add cobs_gpu_index_column_offset for the
+ * file column.  Per query, the union of every shard's hits ordered by
+ * (score desc, name asc) and cut to top_t equals the unsharded result.
+ * COBS_EUSAGE for an empty/out-of-range block range or a classic index
+ * split into parts. */
+int cobs_gpu_index_open_blocks(const char* path, int device, uint64_t block_lo, uint64_t block_hi,
+                               cobs_gpu_index** out, char* err, size_t errlen);
+uint64_t cobs_gpu_index_column_offset(const cobs_gpu_index* index);
+
 /* Same, from an in-memory file image (`path` is only used in messages). */
 int cobs_gpu_index_open_image(const uint8_t* image, uint64_t len, const char* path, int device,
                               cobs_gpu_index** out, char* err, size_t errlen);

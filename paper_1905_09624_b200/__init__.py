@@ -152,6 +152,11 @@ class DeviceIndexView:
     def __exit__(self, *exc):
         self.close()
 
+    def column_offset(self) -> int:
+        """File column of this index's first document (non-zero for a block
+        shard opened with open_blocks)."""
+        return int(N.lib.cobs_gpu_index_column_offset(self._h))
+
     def set_stream(self, stream_ptr: int) -> None:
         """Run this index's batches on a caller-owned cudaStream_t."""
         N.lib.cobs_gpu_index_set_stream(self._h, C.c_void_p(stream_ptr or None))
@@ -228,6 +233,20 @@ def open_random_access(path: str, hbm_budget: int, device: int = 0) -> DeviceInd
     err = _errbuf()
     rc = N.lib.cobs_gpu_index_open_ex(str(path).encode(), device, hbm_budget, C.byref(h), err,
                                       len(err))
+    if rc:
+        _raise(rc, err)
+    return DeviceIndexView(h.value)
+
+
+def open_blocks(path: str, block_lo: int, block_hi: int, device: int = 0) -> DeviceIndexView:
+    """Blocks [block_lo, block_hi) of a compact index file as a standalone
+    compact index in HBM -- one shard of a block-sharded index (SURVEY.md
+    §8e).  Its hit columns are local; column_offset() maps them to file
+    columns.  Merge shard results with dist.merge_block_shards."""
+    h = C.c_void_p()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_index_open_blocks(str(path).encode(), device, block_lo, block_hi, C.byref(h),
+                                          err, len(err))
     if rc:
         _raise(rc, err)
     return DeviceIndexView(h.value)

@@ -80,6 +80,18 @@ int cobs_gpu_index_open_ex(const char* path, int device, uint64_t hbm_budget, co
     });
 }
 
+int cobs_gpu_index_open_blocks(const char* path, int device, uint64_t block_lo, uint64_t block_hi,
+                               cobs_gpu_index** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::open_index_blocks(cobsg::file_source(path), device, block_lo, block_hi);
+        *out = h.release();
+    });
+}
+
+uint64_t cobs_gpu_index_column_offset(const cobs_gpu_index* index) { return index->ix->column_offset; }
+
 int cobs_gpu_index_open_image_ex(const uint8_t* image, uint64_t len, const char* path, int device,
                                  uint64_t hbm_budget, cobs_gpu_index** out, char* err, size_t errlen) {
     *out = nullptr;

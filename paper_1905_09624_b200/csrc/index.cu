@@ -219,6 +219,44 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
 
 } // namespace
 
+namespace {
+
+// Rows of every block into the pitched HBM payload through two pinned
+// staging buffers (re-pitched on the copy engine), the next chunk read from
+// the source while the previous one is copied.  src_offset[b]: file offset of
+// block b's payload.
+void upload_rows(DeviceIndex& ix, const ByteSource& src, const std::vector<uint64_t>& src_offset) {
+    const size_t kStage = 64ull << 20;
+    PinnedBuf stage[2];
+    stage[0].reserve(kStage);
+    stage[1].reserve(kStage);
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+    int cur = 0;
+    bool used[2] = {false, false};
+    for (size_t b = 0; b < ix.blocks.size(); ++b) {
+        const DevBlock& d = ix.blocks[b];
+        uint64_t rows_per = std::max<uint64_t>(1, kStage / d.rb);
+        for (uint64_t r0 = 0; r0 < d.w; r0 += rows_per) {
+            uint64_t rows = std::min(rows_per, d.w - r0);
+            if (used[cur]) COBS_CUDA(cudaEventSynchronize(done[cur]));
+            if (rows * d.rb > stage[cur].bytes) stage[cur].reserve(rows * d.rb);
+            src.read_at(src_offset[b] + r0 * d.rb, stage[cur].ptr, rows * d.rb);
+            uint8_t* dst = ix.payload + d.base + r0 * d.pitch;
+            if (d.pitch == d.rb)
+                COBS_CUDA(cudaMemcpyAsync(dst, stage[cur].ptr, rows * d.rb, cudaMemcpyHostToDevice, ix.stream));
+            else
+                COBS_CUDA(cudaMemcpy2DAsync(dst, d.pitch, stage[cur].ptr, d.rb, d.rb, rows, cudaMemcpyHostToDevice,
+                                            ix.stream));
+            COBS_CUDA(cudaEventRecord(done[cur], ix.stream));
+            used[cur] = true;
+            cur ^= 1;
+        }
+    }
+    COBS_CUDA(cudaStreamSynchronize(ix.stream));
+}
+
+} // namespace
+
 std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget) {
     auto ix = std::make_unique<DeviceIndex>();
     ix->meta = parse_index(src);
@@ -230,37 +268,39 @@ std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint6
         return ix;
     }
     ix->allocate();
-    // Stream rows through two pinned staging buffers, re-pitching on the copy
-    // engine (cudaMemcpy2DAsync), while the next chunk is read from the file.
-    const size_t kStage = 64ull << 20;
-    PinnedBuf stage[2];
-    stage[0].reserve(kStage);
-    stage[1].reserve(kStage);
-    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
-    int cur = 0;
-    bool used[2] = {false, false};
-    for (size_t b = 0; b < ix->blocks.size(); ++b) {
-        const DevBlock& d = ix->blocks[b];
-        const BlockMeta& m = ix->meta.blocks[b];
-        uint64_t rows_per = std::max<uint64_t>(1, kStage / d.rb);
-        for (uint64_t r0 = 0; r0 < d.w; r0 += rows_per) {
-            uint64_t rows = std::min(rows_per, d.w - r0);
-            if (used[cur]) COBS_CUDA(cudaEventSynchronize(done[cur]));
-            if (rows * d.rb > stage[cur].bytes) stage[cur].reserve(rows * d.rb);
-            src.read_at(m.offset + r0 * d.rb, stage[cur].ptr, rows * d.rb);
-            uint8_t* dst = ix->payload + d.base + r0 * d.pitch;
-            if (d.pitch == d.rb)
-                COBS_CUDA(cudaMemcpyAsync(dst, stage[cur].ptr, rows * d.rb, cudaMemcpyHostToDevice,
-                                          ix->stream));
-            else
-                COBS_CUDA(cudaMemcpy2DAsync(dst, d.pitch, stage[cur].ptr, d.rb, d.rb, rows,
-                                            cudaMemcpyHostToDevice, ix->stream));
-            COBS_CUDA(cudaEventRecord(done[cur], ix->stream));
-            used[cur] = true;
-            cur ^= 1;
-        }
+    std::vector<uint64_t> offs;
+    for (const BlockMeta& m : ix->meta.blocks) offs.push_back(m.offset);
+    upload_rows(*ix, src, offs);
+    ix->finish_upload();
+    return ix;
+}
+
+std::unique_ptr<DeviceIndex> open_index_blocks(const ByteSource& src, int device, uint64_t block_lo,
+                                               uint64_t block_hi) {
+    IndexMeta full = parse_index(src);
+    const uint64_t nb = full.blocks.size();
+    if (!(block_lo < block_hi && block_hi <= nb))
+        throw UsageError("open_blocks: block range [" + std::to_string(block_lo) + ", " + std::to_string(block_hi) +
+                         ") outside [0, " + std::to_string(nb) + ")");
+    if (full.kind != kKindCompact && !(block_lo == 0 && block_hi == nb))
+        throw UsageError("open_blocks: block sharding needs a compact index");
+    auto ix = std::make_unique<DeviceIndex>();
+    IndexMeta& m = ix->meta;
+    m.params = full.params;
+    m.kind = full.kind;
+    std::vector<uint64_t> offs;
+    for (uint64_t b = block_lo; b < block_hi; ++b) {
+        const BlockMeta& fb = full.blocks[b];
+        offs.push_back(fb.offset);
+        m.blocks.push_back(fb);
+        m.docs.insert(m.docs.end(), full.docs.begin() + fb.doc_base, full.docs.begin() + fb.doc_base + fb.doc_count);
     }
-    COBS_CUDA(cudaStreamSynchronize(ix->stream));
+    m.layout(); // offsets of the shard as a standalone file (for write / image)
+    ix->column_offset = full.blocks[block_lo].doc_base;
+    ix->device = device;
+    ix->plan();
+    ix->allocate();
+    upload_rows(*ix, src, offs);
     ix->finish_upload();
     return ix;
 }

@@ -92,6 +92,7 @@ struct DeviceIndex {
     uint32_t* d_ct = nullptr; // [2*nct]: block, slice
     uint32_t* d_name_rank = nullptr;
     uint64_t sum_row_bytes = 0; // sum_b row_bytes_b
+    uint64_t column_offset = 0; // block shard: file column of this index's first document
     bool evict_first = false;   // payload far larger than L2
     std::mutex mu;
     QueryWorkspace ws;
@@ -110,6 +111,12 @@ struct DeviceIndex {
 // With hbm_budget > 0 and a pitched payload larger than it, open in the
 // host-resident streaming mode with two staging buffers of hbm_budget/2.
 std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget = 0);
+// Blocks [block_lo, block_hi) of a compact index as a standalone compact
+// index resident in HBM (SURVEY.md §8e block sharding): same params, those
+// blocks and their documents; column_offset = the file column of its first
+// document.  The whole header is parsed and validated as by open_index.
+std::unique_ptr<DeviceIndex> open_index_blocks(const ByteSource& src, int device, uint64_t block_lo,
+                                               uint64_t block_hi);
 // Config-5 procedural index generated in HBM.
 std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n_docs, uint64_t block_size,
                                             double median, double sigma, double p, int device);

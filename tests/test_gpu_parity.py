@@ -480,3 +480,57 @@ def test_count_partitioned_huge_document(gpu):
         for name, content in docs[1:]:
             terms, _, _ = O.ref_extract_terms(content, 31, True)
             assert got[name] == len(terms)
+
+
+def test_block_shards(gpu, tmp_path):
+    """Block sharding: shards opened with open_blocks answer
+    the batch; merged by (score desc, name asc) and cut to top_t they equal
+    the unsharded index, their dense scores concatenate to its dense scores,
+    and a shard written out is the compact index of its blocks."""
+    from paper_1905_09624_b200 import dist as D
+    rng = random.Random(31)
+    docs = [(b"s%04d" % rng.randrange(10000), [rand(rng, rng.randrange(50, 3000))]) for _ in range(70)]
+    docs = list({n: (n, c) for n, c in docs}.values())
+    params = cb.IndexParams(block_size=8, canonical=True)
+    path = str(tmp_path / "sharded.cobs")
+    img = cb.build_compact(docs, params, path=path, device=gpu)
+    full = cb.open_resident(path, gpu)
+    nb = full.block_count()
+    cuts = [0, 2, 5, nb]
+    shards = [cb.open_blocks(path, a, b, gpu) for a, b in zip(cuts, cuts[1:])]
+    assert [s.column_offset() for s in shards] == [sum(full.doc_count(b) for b in range(c)) for c in cuts[:-1]]
+    pats = [d[1][0][10:400] for d in docs[::5]] + [rand(rng, 300), b"ACG"]
+    for K, top_t in ((0.3, 0), (0.3, 4), (1e-12, 0), (0.9, 1)):
+        want = cb.query_batch(full, pats, K, top_t, scores=(top_t == 0))
+        parts = [cb.query_batch(s, pats, K, top_t, scores=(top_t == 0)) for s in shards]
+        merged = D.merge_block_shards([D.shard_hits(r, s.doc_names(), s.column_offset())
+                                       for r, s in zip(parts, shards)], top_t)
+        for i in range(len(pats)):
+            d, sc = want.hits(i)
+            assert [(a, b) for a, b, _ in merged[i]] == [(int(x), int(y)) for x, y in zip(d, sc)], (K, top_t, i)
+            for r in parts:
+                assert r.ell[i] == want.ell[i] and r.status[i] == want.status[i]
+        if top_t == 0:
+            assert np.array_equal(np.concatenate([r.dense for r in parts], axis=1), want.dense)
+    # a shard is itself a compact index of its blocks
+    idx = O.OracleIndex.parse(img)
+    shard_img = cb.index_image(shards[1])
+    sidx = O.OracleIndex.parse(shard_img)
+    assert [(dc, w) for dc, w, _ in sidx.blocks()] == [(dc, w) for dc, w, _ in idx.blocks()[2:5]]
+    lo = idx.blocks()[2][2]
+    assert sidx.names() == idx.names()[lo:lo + len(sidx.names())]
+    for b in range(3):
+        for r in (0, shards[1].width(b) - 1):
+            assert shards[1].row_data(b, r) == full.row_data(b + 2, r)
+    # errors: empty / out-of-range block ranges, a classic index split
+    for a, b in ((3, 3), (0, nb + 1), (nb, nb + 1)):
+        with pytest.raises(ValueError, match="open_blocks"):
+            cb.open_blocks(path, a, b, gpu)
+    cpath = str(tmp_path / "classic.cobs")
+    cb.build_classic(docs[:10], cb.IndexParams(), path=cpath, device=gpu)
+    with pytest.raises(ValueError, match="open_blocks"):
+        cb.open_blocks(cpath, 0, 2, gpu)
+    cb.open_blocks(cpath, 0, 1, gpu).close()  # a classic index is one block: the whole index
+    for s in shards:
+        s.close()
+    full.close()
