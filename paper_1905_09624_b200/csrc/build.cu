@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) pc_dedup_kernel(const uint32_t* off, uint
     for (uint64_t t = blockIdx.x; t < nbuckets; t += gridDim.x) {
         const uint32_t o0 = off[t], o1 = off[t + 1];
         if (o0 == o1) continue; // uniform over the CTA
-        uint32_t S = 64, S_log2 = 6;
+        uint32_t S = 64, S_log2 = 6; // (>= 16 groups of 4)
         while (S < 2 * (o1 - o0) && S < slots) {
             S <<= 1;
             ++S_log2;
@@ -392,25 +392,32 @@ __global__ void __launch_bounds__(256) pc_dedup_kernel(const uint32_t* off, uint
         __syncthreads();
         uint32_t mine = 0;
         bool stuck = false;
+        // Bucketised set: S/4 groups of 4 slots (32 bytes, two LDS.128); a key
+        // is looked up in its group with straight-line compares and claims the
+        // group's first empty slot, so most keys finish in one round.  Keys of
+        // a bucket are codes spread by the bucket's mix, so a 32-bit
+        // multiplicative hash suffices for the group.
+        const uint32_t G = S / 4;
         auto insert = [&](unsigned long long key) {
-            // keys of a bucket are codes spread by the bucket's mix, so a
-            // 32-bit multiplicative hash suffices for the slot
-            uint32_t slot = ((static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * 0x9E3779B1u) >> (32 - S_log2);
-            for (uint32_t probes = 0;; slot = (slot + 1) & (S - 1)) {
-                if (++probes > S) {
-                    stuck = true;
-                    return;
-                }
-                unsigned long long cur = s_tab[slot];
-                if (cur == 0ull) {
-                    cur = atomicCAS(&s_tab[slot], 0ull, key);
+            uint32_t g = ((static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * 0x9E3779B1u) >> (34 - S_log2);
+            for (uint32_t probes = 0; probes < G; ++probes, g = (g + 1) & (G - 1)) {
+                unsigned long long* grp = s_tab + 4 * g;
+                const ulonglong2 lo = *reinterpret_cast<const ulonglong2*>(grp);
+                const ulonglong2 hi = *reinterpret_cast<const ulonglong2*>(grp + 2);
+                if (lo.x == key || lo.y == key || hi.x == key || hi.y == key) return;
+                unsigned long long v[4] = {lo.x, lo.y, hi.x, hi.y};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (v[e] != 0ull) continue;
+                    const unsigned long long cur = atomicCAS(grp + e, 0ull, key);
                     if (cur == 0ull) {
                         ++mine;
                         return;
                     }
+                    if (cur == key) return;
                 }
-                if (cur == key) return;
             }
+            stuck = true; // every group full: the wave is recounted
         };
         // 8 independent key loads in flight per thread, then the inserts
         for (uint32_t i0 = o0 + threadIdx.x; i0 < o1; i0 += 8 * blockDim.x) {
