@@ -116,13 +116,17 @@ def test_c1_full_vs_reference(gpu, tmp_path):
 
 
 @pytest.mark.skipif(os.environ.get("COBS_SKIP_C5_FULL") == "1", reason="disabled")
-def test_c5_full_sample(gpu):
-    """Full-size config 5 (~100 GB in HBM): sampled rows equal the host
-    generator; a seeded sample of the batch's queries scores exactly as the
-    oracle over the procedural index."""
+@pytest.mark.parametrize("median", [None, 4.5e6], ids=["c5", "c5_literal_median"])
+def test_c5_full_sample(gpu, median):
+    """Full-size config 5 (~100 GB in HBM; and the literal 4.5 M median, a
+    185 GB index): sampled rows equal the host generator; a seeded sample of
+    the batch's queries scores exactly as the oracle over the procedural
+    index."""
     cfg = synth.CONFIGS["c5"]
+    if median:
+        cfg = synth.replace(cfg, c5_median=median)
     view = cb.synth_c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p)
-    assert view.device_bytes() > 90e9
+    assert view.device_bytes() > (180e9 if median else 90e9)
     orc = O.OracleIndex.c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p)
     blocks = orc.blocks()
     assert [(view.doc_count(b), view.width(b)) for b in range(view.block_count())] == \
