@@ -1,21 +1,26 @@
 // Kernel 4: index construction on the device.
 //
-//   count pass  one thread per window (flattened over all documents, so
-//               skewed document sizes load-balance): canonicalise, XXH64,
-//               exact per-document distinct count through the lock-free set
-//               of dev.cuh -> term_count   (termizer.cpp:103-129,
-//               termizer.hpp:25)
+//   count pass  exact per-document distinct count -> term_count
+//               (termizer.cpp:103-129, termizer.hpp:25), windows rolled as
+//               2-bit codes (canonical = min(fwd, revcomp)):
+//               * partitioned (q <= 32, large corpora): codes split by a
+//                 bijective mix into per-document buckets (shared-memory
+//                 histograms, scan, scatter), each bucket deduplicated in a
+//                 shared-memory set -- pc_*_kernel;
+//               * hash sets (any q, byte-path windows, small corpora):
+//                 per-document lock-free sets in L2-sized waves -- count_kernel.
 //   host        classic width / compact (term_count, name) sort, blocks of
 //               B, per-block widths        (classic_index.cpp:40-64,
 //               compact_index.cpp:19-52, bloom.cpp:50-66)
 //   fill pass   for every window and seed, bit (XXH64 % w_b, column)
 //               (classic_index.cpp:26-36, bit_matrix.hpp:25-27): 32
 //               consecutive columns of a block are one u32 per row, so waves
-//               of such column "slabs" (L2-sized) are filled with atomicOr and
-//               then copied into the pitched HBM layout of the query index
-//               (a built index is queryable in place; the file payload is its
-//               un-pitched D2H copy).  OR is idempotent, so every window is
-//               filled, not just the distinct ones.
+//               of such column "slabs" (L2-sized) are filled with atomicOr,
+//               then copied 8 groups (32 bytes per row) at a time into the
+//               pitched HBM layout of the query index (a built index is
+//               queryable in place; the file payload is its un-pitched D2H
+//               copy).  OR is idempotent, so every window is filled, not just
+//               the distinct ones.
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
