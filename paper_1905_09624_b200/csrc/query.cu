@@ -255,6 +255,7 @@ struct GatherArgs {
     uint64_t n;
     uint32_t k;
     uint32_t qt; // queries per tile (multiple of 8)
+    uint32_t split; // 1: one warp per (query, column task); 8: the CTA's 8 warps split one query's terms
     uint64_t D;
     void* scores; // dense [n][D] (uint16 or uint32) or null
     int want_hits;
@@ -375,14 +376,20 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
     __shared__ __align__(16) RowT s_rows[8][KS * CH];
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t groups = (a.qt + 7) / 8;
+    // split = 8 (small batches): the CTA's warps take every 8th chunk of one
+    // query's terms and their counts are added at the end (more warps in
+    // flight per query when there are too few queries to fill the GPU)
+    const uint32_t S = a.split;
+    const uint32_t qpc = S == 1 ? 8u : 1u; // queries per CTA
+    const uint32_t groups = (a.qt + qpc - 1) / qpc;
     const uint32_t per_tile = groups * a.nct;
     const uint32_t bid = blockIdx.x;
     const uint32_t tile = bid / per_tile;
     const uint32_t r = bid - tile * per_tile;
     const uint32_t cti = r / groups;
     const uint32_t qg = r - cti * groups;
-    const uint32_t qin = qg * 8 + warp;
+    const uint32_t qin = S == 1 ? qg * 8 + warp : qg;
+    const uint32_t sub = S == 1 ? 0u : warp; // this warp's first chunk
     const uint64_t qi = static_cast<uint64_t>(tile) * a.qt + qin;
     if (qin >= a.qt || qi >= a.n) return;
     const uint32_t ell = a.ell[qi];
@@ -404,10 +411,12 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
 #pragma unroll
     for (int p = 0; p < NPP; ++p) P[p] = 0;
 
+    const uint32_t stride = S * CH; // terms from one of this warp's chunks to its next
     uint64_t hnext[KS];
 #pragma unroll
     for (int s = 0; s < KS; ++s)
-        hnext[s] = (KT != 0 && lane < CH && lane < ell) ? __ldg(hq + (uint64_t)lane * KS + s) : 0;
+        hnext[s] = (KT != 0 && lane < CH && sub * CH + lane < ell) ? __ldg(hq + (uint64_t)(sub * CH + lane) * KS + s)
+                                                                   : 0;
     // One chunk of CH terms; TAIL (the last, partial chunk only) zeroes the
     // masks of the padding terms, so full chunks carry no per-term predicate.
     auto chunk = [&](uint32_t t0, auto tail_c) {
@@ -418,9 +427,9 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
             uint64_t h[KS];
 #pragma unroll
             for (int s = 0; s < KS; ++s) h[s] = hnext[s];
-            if (lane < CH && tl + CH < ell) { // prefetch the next chunk's hashes
+            if (lane < CH && tl + stride < ell) { // prefetch the next chunk's hashes
 #pragma unroll
-                for (int s = 0; s < KS; ++s) hnext[s] = __ldg(hq + (uint64_t)(tl + CH) * KS + s);
+                for (int s = 0; s < KS; ++s) hnext[s] = __ldg(hq + (uint64_t)(tl + stride) * KS + s);
             }
             if (lane < CH) {
 #pragma unroll
@@ -501,13 +510,13 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
         add_at<NT>(F, 0, ones);
     };
 
-    uint32_t t0 = 0;
-    for (; t0 + CH <= ell; t0 += CH) {
+    uint32_t t0 = sub * CH;
+    for (; t0 + CH <= ell; t0 += stride) {
         chunk(t0, std::false_type{});
         // Optional threshold pruning (hits only): every 2 chunks, if no document
         // of this slice can still reach tau with all remaining terms, its hit
         // list is empty whatever those rows hold -- stop reading them.
-        if (a.prune && ((t0 / CH) & 1u) == 1u) {
+        if (a.prune && S == 1 && ((t0 / CH) & 1u) == 1u) {
             const uint32_t rem = ell - (t0 + CH);
             if (tau > rem) {
                 flush();
@@ -515,8 +524,26 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
             }
         }
     }
-    if (t0 < ell) chunk(t0, std::true_type{});
+    if (t0 < ell) chunk(t0, std::true_type{}); // the partial last chunk, if it is this warp's
     flush();
+    if (S > 1) { // add the warps' counts: bit-sliced ripple-carry adds in warp 0
+        extern __shared__ uint32_t s_planes[]; // [8][NT][32]
+#pragma unroll
+        for (int p = 0; p < NT; ++p) s_planes[(warp * NT + p) * 32 + lane] = F[p];
+        __syncthreads();
+        if (warp != 0) return;
+        for (uint32_t w = 1; w < 8; ++w) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int p = 0; p < NT; ++p) {
+                const uint32_t g = s_planes[(w * NT + p) * 32 + lane];
+                const uint32_t x = F[p] ^ g;
+                const uint32_t sum = x ^ c;
+                c = (F[p] & g) | (x & c);
+                F[p] = sum;
+            }
+        }
+    }
 
     if (a.scores) {
         if (NT <= 16) {
@@ -762,8 +789,14 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     bool w32 = true;
     for (const DevBlock& d : ix.blocks) w32 &= d.w <= 0xffffffffull;
     GatherFn fn = pick_gather(nt_needed, (w32 && k <= 3) ? static_cast<int>(k) : 0, ix.evict_first);
+    // Term split for batches too small to fill the GPU with one warp per
+    // (query, column task): fewer than ~4 resident waves of warps.
+    ga.split = static_cast<uint64_t>(n) * ga.nct < 4ull * 148 * 24 ? 8 : 1;
+    if (const char* e = std::getenv("COBS_SPLIT")) ga.split = std::strtoul(e, nullptr, 10) == 8 ? 8 : 1;
+    const uint32_t qpc = ga.split == 1 ? 8 : 1;
+    const size_t split_smem = ga.split == 1 ? 0 : 8 * 32 * 32 * 4; // [8 warps][NT <= 32][32 lanes]
     const uint64_t tiles = (n + qt - 1) / qt;
-    const uint64_t grid2 = tiles * ((qt + 7) / 8) * ga.nct;
+    const uint64_t grid2 = tiles * ((qt + qpc - 1) / qpc) * ga.nct;
     if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
     unsigned long long h_total = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -776,7 +809,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
         if (attempt == 0) COBS_CUDA(cudaEventRecord(ev[1], st));
         if (!ix.streaming()) {
             if (grid2 > 0) {
-                fn<<<static_cast<unsigned>(grid2), 256, 0, st>>>(ga);
+                fn<<<static_cast<unsigned>(grid2), 256, split_smem, st>>>(ga);
                 R.launches += 1;
             }
         } else { // host-resident index: stream slab groups through two staging buffers
@@ -804,10 +837,10 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
                 gg.blocks = hs.d_slab_blocks;
                 gg.ct = hs.d_slab_ct + 2ull * G.ct_lo;
                 gg.nct = G.ct_hi - G.ct_lo;
-                const uint64_t grid_g = tiles * ((qt + 7) / 8) * gg.nct;
+                const uint64_t grid_g = tiles * ((qt + qpc - 1) / qpc) * gg.nct;
                 if (grid_g >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
                 if (grid_g > 0) {
-                    fn<<<static_cast<unsigned>(grid_g), 256, 0, st>>>(gg);
+                    fn<<<static_cast<unsigned>(grid_g), 256, split_smem, st>>>(gg);
                     R.launches += 1;
                 }
                 COBS_CUDA(cudaEventRecord(hs.consumed[buf], st));

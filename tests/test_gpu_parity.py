@@ -534,3 +534,34 @@ def test_block_shards(gpu, tmp_path):
     for s in shards:
         s.close()
     full.close()
+
+
+def test_term_split_equals_warp_per_query(gpu):
+    """Small batches split one query's terms over a CTA's 8 warps and add the
+    bit-sliced counts (COBS_SPLIT=8); dense scores, l and hit lists are
+    identical to the one-warp-per-query kernel (COBS_SPLIT=1), for k = 1..4
+    and ℓ around the chunk sizes, and equal the oracle."""
+    rng = random.Random(12)
+    docs = [(b"t%03d" % i, [rand(rng, rng.randrange(100, 5000))]) for i in range(300)]
+    for k, canonical in ((1, False), (2, True), (3, False), (4, False)):
+        img = cb.build_compact(docs, cb.IndexParams(q=31, k=k, canonical=canonical, block_size=100), device=gpu)
+        view = cb.open_image(img, gpu)
+        idx = O.OracleIndex.parse(img)
+        pats = [docs[rng.randrange(300)][1][0][:L] for L in (31, 32, 62, 63, 64, 95, 287, 288, 1000)
+                if len(docs[0][1][0]) >= 0] + [rand(rng, 2000)]
+        pats = [p for p in pats if len(p) >= 31]
+        out = {}
+        for split in ("1", "8"):
+            os.environ["COBS_SPLIT"] = split
+            try:
+                out[split] = cb.query_batch(view, pats, 0.2, scores=True)
+            finally:
+                os.environ.pop("COBS_SPLIT", None)
+        a, b = out["1"], out["8"]
+        assert np.array_equal(a.dense, b.dense) and np.array_equal(a.ell, b.ell)
+        assert np.array_equal(a.hit_n, b.hit_n) and np.array_equal(a.docs, b.docs)
+        assert np.array_equal(a.scores, b.scores)
+        for i, p in enumerate(pats):
+            e, s, h, dense = idx.query(p, 0.2, scores=True)
+            assert np.array_equal(b.dense[i].astype(np.uint32), dense), (k, i)
+        view.close()

@@ -40,7 +40,9 @@ def main():
             ts.append((time.perf_counter() - t) * 1e3)
         med = statistics.median(ts)
         res["batches"].append({"queries": n, "ms_median": med, "ms_min": min(ts),
-                               "ms_device_total": r.ms_total, "queries_per_s": n / (med / 1e3),
+                               "ms_device_total": r.ms_total, "ms_termize": r.ms_termize,
+                               "ms_gather": r.ms_gather, "ms_order": r.ms_order,
+                               "queries_per_s": n / (med / 1e3),
                                "launches": r.launches})
         print(json.dumps(res["batches"][-1]), flush=True)
     view.close()
