@@ -638,11 +638,12 @@ GatherFn pick_gather(int nt_needed, int kt, bool ef) {
 
 } // namespace
 
-void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offsets, uint64_t n,
-                 double K, uint64_t top_t, uint32_t flags, QueryResults& R) {
-    if (!(K > 0.0 && K <= 1.0)) throw UsageError("query: K must be in (0,1]"); // query.cpp:125
-    std::lock_guard<std::mutex> lock(ix.mu);
-    COBS_CUDA(cudaSetDevice(ix.device));
+namespace {
+
+// One batch through kernels 1-3; the caller holds ix.mu.  min_nt: at least
+// this many count bits (dense score width agreed over sub-batches).
+void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offsets, uint64_t n,
+                     double K, uint64_t top_t, uint32_t flags, int min_nt, QueryResults& R) {
     QueryWorkspace& ws = ix.ws;
     cudaStream_t st = ix.work_stream();
     const Params& P = ix.meta.params;
@@ -753,7 +754,7 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     // kernel 2
     const bool want_scores = flags & COBS_Q_SCORES;
     const bool want_hits = (flags & COBS_Q_HITS) || !(flags & COBS_Q_SCORES);
-    int nt_needed = bits_for(wmax);
+    int nt_needed = std::max(bits_for(wmax), min_nt);
     R.score_bytes = nt_needed <= 16 ? 2 : 4;
     if (want_scores) {
         ws.scores.reserve(std::max<uint64_t>(n * D * R.score_bytes, 1));
@@ -953,6 +954,79 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     float ttot = 0;
     cudaEventElapsedTime(&ttot, ev_begin, ev_end);
     R.ms_total = ttot;
+}
+
+void append_results(QueryResults& R, QueryResults&& S) {
+    const uint64_t base = R.doc.size();
+    R.n += S.n;
+    R.ell.insert(R.ell.end(), S.ell.begin(), S.ell.end());
+    R.tau.insert(R.tau.end(), S.tau.begin(), S.tau.end());
+    R.skipped.insert(R.skipped.end(), S.skipped.begin(), S.skipped.end());
+    R.status.insert(R.status.end(), S.status.begin(), S.status.end());
+    for (auto& m : S.message) R.message.push_back(std::move(m));
+    for (uint64_t o : S.hit_off) R.hit_off.push_back(o + base);
+    R.hit_n.insert(R.hit_n.end(), S.hit_n.begin(), S.hit_n.end());
+    R.doc.insert(R.doc.end(), S.doc.begin(), S.doc.end());
+    R.score.insert(R.score.end(), S.score.begin(), S.score.end());
+    R.scores.insert(R.scores.end(), S.scores.begin(), S.scores.end());
+    R.score_bytes = S.score_bytes;
+    R.ms_termize += S.ms_termize;
+    R.ms_gather += S.ms_gather;
+    R.ms_order += S.ms_order;
+    R.ms_total += S.ms_total;
+    R.launches += S.launches;
+    R.h2d_index_bytes += S.h2d_index_bytes;
+    R.row_bytes += S.row_bytes;
+}
+
+} // namespace
+
+// A host batch whose per-window buffers (hashes, sets) and dense scores would
+// not fit in half of the free HBM is run as consecutive sub-batches and the
+// results concatenated (same answers, same dense score width).
+void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offsets, uint64_t n,
+                 double K, uint64_t top_t, uint32_t flags, QueryResults& R) {
+    if (!(K > 0.0 && K <= 1.0)) throw UsageError("query: K must be in (0,1]"); // query.cpp:125
+    std::lock_guard<std::mutex> lock(ix.mu);
+    COBS_CUDA(cudaSetDevice(ix.device));
+    if ((flags & (COBS_Q_DEVICE_INPUT | COBS_Q_KEEP_DEVICE)) || n <= 1) {
+        query_batch_one(ix, patterns, offsets, n, K, top_t, flags, 1, R);
+        return;
+    }
+    const uint32_t q = ix.meta.params.q, k = ix.meta.params.k;
+    const uint64_t D = ix.meta.total_docs();
+    const bool want_scores = flags & COBS_Q_SCORES;
+    std::vector<uint64_t> cost(n); // device bytes per query, roughly
+    uint64_t total = 0, wmax = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t len = offsets[i + 1] - offsets[i];
+        const uint64_t W = len >= q ? len - q + 1 : 0;
+        wmax = std::max(wmax, W);
+        cost[i] = len + W * (8ull * k + 24) + (want_scores ? 4 * D : 0) + 64;
+        total += cost[i];
+    }
+    size_t free_b = 0, total_b = 0;
+    COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t budget = std::max<uint64_t>(free_b / 2, 64ull << 20);
+    if (const char* e = std::getenv("COBS_QUERY_BUDGET")) budget = std::strtoull(e, nullptr, 10);
+    if (total <= budget) {
+        query_batch_one(ix, patterns, offsets, n, K, top_t, flags, 1, R);
+        return;
+    }
+    const int nt = bits_for(wmax);
+    R = QueryResults();
+    std::vector<uint64_t> sub_off;
+    for (uint64_t a = 0; a < n;) {
+        uint64_t b = a, c = 0;
+        while (b < n && (b == a || c + cost[b] <= budget)) c += cost[b++];
+        sub_off.assign(offsets + a, offsets + b + 1);
+        const uint64_t base = sub_off[0];
+        for (uint64_t& o : sub_off) o -= base;
+        QueryResults S;
+        query_batch_one(ix, patterns + base, sub_off.data(), b - a, K, top_t, flags, nt, S);
+        append_results(R, std::move(S));
+        a = b;
+    }
 }
 
 } // namespace cobsg

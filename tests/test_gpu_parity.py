@@ -565,3 +565,34 @@ def test_term_split_equals_warp_per_query(gpu):
             e, s, h, dense = idx.query(p, 0.2, scores=True)
             assert np.array_equal(b.dense[i].astype(np.uint32), dense), (k, i)
         view.close()
+
+
+def test_sub_batches_equal_one_batch(gpu):
+    """A host batch larger than the device budget runs as consecutive
+    sub-batches (forced here with COBS_QUERY_BUDGET): hit lists, l, skipped,
+    messages and dense scores -- including the 32-bit score width a single
+    long pattern forces on the whole batch -- equal the one-batch answer."""
+    rng = random.Random(21)
+    docs = [(b"u%03d" % i, [rand(rng, rng.randrange(200, 3000))]) for i in range(120)]
+    docs.append((b"long", [rand(rng, 70000)]))
+    img = cb.build_compact(docs, cb.IndexParams(block_size=50), device=gpu)
+    view = cb.open_image(img, gpu)
+    pats = [docs[rng.randrange(len(docs))][1][0][:rng.randrange(20, 900)] for _ in range(60)]
+    pats.insert(17, docs[-1][1][0][:66000])  # l > 65535: 32-bit scores for every query
+    pats.insert(3, b"ACG")                    # DataError row
+    one = cb.query_batch(view, pats, 0.3, 5, scores=True)
+    os.environ["COBS_QUERY_BUDGET"] = "300000"
+    try:
+        split = cb.query_batch(view, pats, 0.3, 5, scores=True)
+    finally:
+        os.environ.pop("COBS_QUERY_BUDGET")
+    assert split.launches > one.launches  # really ran as several sub-batches
+    assert one.dense.dtype == split.dense.dtype == np.uint32
+    assert np.array_equal(one.dense, split.dense)
+    for f in ("ell", "skipped", "status", "hit_n"):
+        assert np.array_equal(getattr(one, f), getattr(split, f)), f
+    assert one.messages == split.messages
+    for i in range(len(pats)):
+        a, b = one.hits(i), split.hits(i)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    view.close()
