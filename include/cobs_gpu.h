@@ -79,6 +79,15 @@ int cobs_gpu_index_open_image_ex(const uint8_t* image, uint64_t len, const char*
 /* 1 if the index is in the host-resident streaming mode. */
 int cobs_gpu_index_streaming(const cobs_gpu_index* index);
 
+/* cobs::open_random_access (storage.hpp:23, storage.cpp:320-341) in its own
+ * spirit: when the pitched payload exceeds hbm_budget the payload is NOT
+ * copied to host memory -- every batch reads it from the file (host
+ * threads, pread + repack into pinned group images) and streams it through
+ * two HBM staging buffers, so indexes larger than host RAM work too.
+ * Within the budget the index is resident, as cobs_gpu_index_open. */
+int cobs_gpu_index_open_file(const char* path, int device, uint64_t hbm_budget, cobs_gpu_index** out,
+                             char* err, size_t errlen);
+
 /* Block sharding of a compact index (the reference has no
  * sharded reader): blocks [block_lo, block_hi) of the file at `path` as a
  * standalone compact index in HBM -- same params, those blocks and their

@@ -226,13 +226,16 @@ def open_resident(path: str, device: int = 0) -> DeviceIndexView:
     return DeviceIndexView(h.value)
 
 
-def open_random_access(path: str, hbm_budget: int, device: int = 0) -> DeviceIndexView:
-    """Host-resident streaming mode when the pitched payload exceeds
-    hbm_budget (the counterpart of cobs::open_random_access, storage.hpp:23)."""
+def open_random_access(path: str, hbm_budget: int, device: int = 0,
+                       from_file: bool = False) -> DeviceIndexView:
+    """Streaming mode when the pitched payload exceeds hbm_budget (the
+    counterpart of cobs::open_random_access, storage.hpp:23): the payload in
+    pinned host memory, or with from_file=True read from the file every
+    batch (no host copy)."""
     h = C.c_void_p()
     err = _errbuf()
-    rc = N.lib.cobs_gpu_index_open_ex(str(path).encode(), device, hbm_budget, C.byref(h), err,
-                                      len(err))
+    fn = N.lib.cobs_gpu_index_open_file if from_file else N.lib.cobs_gpu_index_open_ex
+    rc = fn(str(path).encode(), device, hbm_budget, C.byref(h), err, len(err))
     if rc:
         _raise(rc, err)
     return DeviceIndexView(h.value)

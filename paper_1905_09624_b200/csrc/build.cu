@@ -1056,7 +1056,7 @@ std::vector<uint8_t> index_image(const DeviceIndex& ix) {
     std::vector<uint8_t> image(header.size() + payload);
     std::memcpy(image.data(), header.data(), header.size());
     if (ix.streaming()) { // host-resident: the payload is already in file layout
-        std::memcpy(image.data() + header.size(), ix.hs->host, payload);
+        ix.hs->read_payload(0, image.data() + header.size(), payload);
         return image;
     }
     COBS_CUDA(cudaSetDevice(ix.device));

@@ -80,6 +80,16 @@ int cobs_gpu_index_open_ex(const char* path, int device, uint64_t hbm_budget, co
     });
 }
 
+int cobs_gpu_index_open_file(const char* path, int device, uint64_t hbm_budget, cobs_gpu_index** out,
+                             char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::open_index(cobsg::file_source(path), device, hbm_budget, /*file_backed=*/true);
+        *out = h.release();
+    });
+}
+
 int cobs_gpu_index_open_blocks(const char* path, int device, uint64_t block_lo, uint64_t block_hi,
                                cobs_gpu_index** out, char* err, size_t errlen) {
     *out = nullptr;
@@ -184,7 +194,7 @@ int cobs_gpu_index_row(const cobs_gpu_index* index, uint64_t b, uint64_t r, uint
         if (b >= ix.blocks.size() || r >= ix.blocks[b].w || lo > hi || hi > ix.blocks[b].rb)
             throw cobsg::UsageError("row: out of range");
         if (ix.streaming()) {
-            std::memcpy(out, ix.hs->host + ix.hs->block_off[b] + r * ix.blocks[b].rb + lo, hi - lo);
+            ix.hs->read_payload(ix.hs->block_off[b] + r * ix.blocks[b].rb + lo, out, hi - lo);
             return;
         }
         COBS_CUDA(cudaSetDevice(ix.device));
@@ -203,9 +213,14 @@ int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* er
         std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
         if (std::fwrite(head.data(), 1, head.size(), f) != head.size())
             throw cobsg::DataError(std::string("error writing index file: ") + path);
-        if (ix.streaming()) {
-            if (std::fwrite(ix.hs->host, 1, ix.hs->host_bytes, f) != ix.hs->host_bytes)
-                throw cobsg::DataError(std::string("error writing index file: ") + path);
+        if (ix.streaming()) { // payload in file layout: host copy or the source file
+            std::vector<uint8_t> chunk(std::min<uint64_t>(ix.hs->host_bytes, 64ull << 20));
+            for (uint64_t o = 0; o < ix.hs->host_bytes; o += chunk.size()) {
+                const uint64_t len = std::min<uint64_t>(chunk.size(), ix.hs->host_bytes - o);
+                ix.hs->read_payload(o, chunk.data(), len);
+                if (std::fwrite(chunk.data(), 1, len, f) != len)
+                    throw cobsg::DataError(std::string("error writing index file: ") + path);
+            }
             return;
         }
         std::vector<uint8_t> buf;

@@ -1,8 +1,11 @@
 // Device-resident index: open (parse + pitched HBM upload) and the config-5
 // procedural generator.  The HBM layout is described in DESIGN.md §3.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <exception>
 #include <numeric>
+#include <thread>
 
 #include "index.hpp"
 #include "synth.h"
@@ -58,7 +61,70 @@ HostStream::~HostStream() {
     if (d_slab_blocks) cudaFree(d_slab_blocks);
     if (d_slab_ct) cudaFree(d_slab_ct);
     if (host) cudaFreeHost(host);
+    for (int i = 0; i < 2; ++i) {
+        if (hstage[i]) cudaFreeHost(hstage[i]);
+        if (h2d_done[i]) cudaEventDestroy(h2d_done[i]);
+    }
     if (copy) cudaStreamDestroy(copy);
+}
+
+void HostStream::read_payload(uint64_t off, void* dst, uint64_t len) const {
+    if (file_backed)
+        src.read_at(payload_start + off, dst, len);
+    else
+        std::memcpy(dst, host + off, len);
+}
+
+void HostStream::stage_group(const std::vector<DevBlock>& blocks, size_t gi, uint8_t* dst) const {
+    // work items: (slab, byte range of a direct slab | row range of a window slab)
+    struct Item {
+        uint32_t slab;
+        uint64_t lo, hi;
+    };
+    constexpr uint64_t kPiece = 8ull << 20;
+    std::vector<Item> items;
+    const StreamGroup& G = groups[gi];
+    for (uint32_t si = G.slab_lo; si < G.slab_hi; ++si) {
+        const Slab& sl = slabs[si];
+        const DevBlock& d = blocks[sl.block];
+        if (sl.direct) {
+            for (uint64_t o = 0; o < d.w * d.rb; o += kPiece) items.push_back({si, o, std::min(d.w * d.rb, o + kPiece)});
+        } else {
+            const uint64_t rows = std::max<uint64_t>(1, kPiece / d.rb);
+            for (uint64_t r = 0; r < d.w; r += rows) items.push_back({si, r, std::min(d.w, r + rows)});
+        }
+    }
+    std::atomic<size_t> next{0};
+    std::exception_ptr failure;
+    std::mutex fail_mu;
+    auto work = [&] {
+        std::vector<uint8_t> tmp;
+        try {
+            for (size_t i = next.fetch_add(1); i < items.size(); i = next.fetch_add(1)) {
+                const Item& it = items[i];
+                const Slab& sl = slabs[it.slab];
+                const DevBlock& d = blocks[sl.block];
+                if (sl.direct) {
+                    read_payload(block_off[sl.block] + it.lo, dst + sl.base + it.lo, it.hi - it.lo);
+                } else { // whole rows from the file, this slab's column window into the image
+                    tmp.resize((it.hi - it.lo) * d.rb);
+                    read_payload(block_off[sl.block] + it.lo * d.rb, tmp.data(), tmp.size());
+                    for (uint64_t r = it.lo; r < it.hi; ++r)
+                        std::memcpy(dst + sl.base + r * sl.pitch, tmp.data() + (r - it.lo) * d.rb + sl.s0 * 128ull,
+                                    sl.width);
+                }
+            }
+        } catch (...) {
+            std::lock_guard<std::mutex> g(fail_mu);
+            failure = std::current_exception();
+        }
+    };
+    const size_t nt = std::min<size_t>(items.size(), std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    if (failure) std::rethrow_exception(failure);
 }
 
 void DeviceIndex::plan() {
@@ -140,14 +206,20 @@ namespace {
 // Host-resident mode: read the payload into pinned memory, cut blocks into
 // slabs of whole 1,024-document slices that fit half the budget, pack slabs
 // into groups (one staging buffer each), upload the slab tables.
-void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
+void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget, bool file_backed) {
     auto hs = std::make_unique<HostStream>();
     const IndexMeta& m = ix.meta;
     hs->host_bytes = m.file_size - m.payload_start;
-    COBS_CUDA(cudaHostAlloc(&hs->host, std::max<uint64_t>(hs->host_bytes, 1), cudaHostAllocDefault));
-    for (uint64_t o = 0; o < hs->host_bytes; o += (1ull << 30)) {
-        uint64_t len = std::min<uint64_t>(1ull << 30, hs->host_bytes - o);
-        src.read_at(m.payload_start + o, hs->host + o, len);
+    hs->payload_start = m.payload_start;
+    hs->file_backed = file_backed;
+    if (file_backed) {
+        hs->src = src;
+    } else {
+        COBS_CUDA(cudaHostAlloc(&hs->host, std::max<uint64_t>(hs->host_bytes, 1), cudaHostAllocDefault));
+        for (uint64_t o = 0; o < hs->host_bytes; o += (1ull << 30)) {
+            uint64_t len = std::min<uint64_t>(1ull << 30, hs->host_bytes - o);
+            src.read_at(m.payload_start + o, hs->host + o, len);
+        }
     }
     const uint64_t half = (budget / 2) & ~255ull;
     hs->staging_bytes = half;
@@ -179,6 +251,7 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
                 g.slab_hi = static_cast<uint32_t>(hs->slabs.size());
                 g.ct_hi = static_cast<uint32_t>(sct.size() / 2);
                 hs->groups.push_back(g);
+                hs->group_bytes.push_back(used);
                 g = StreamGroup{g.slab_hi, 0, g.ct_hi, 0};
                 used = 0;
             }
@@ -201,13 +274,20 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget) {
     }
     g.slab_hi = static_cast<uint32_t>(hs->slabs.size());
     g.ct_hi = static_cast<uint32_t>(sct.size() / 2);
-    if (g.slab_hi > g.slab_lo) hs->groups.push_back(g);
+    if (g.slab_hi > g.slab_lo) {
+        hs->groups.push_back(g);
+        hs->group_bytes.push_back(used);
+    }
     COBS_CUDA(cudaMalloc(&hs->d_slab_blocks, sizeof(DevBlock) * std::max<size_t>(sblocks.size(), 1)));
     COBS_CUDA(cudaMalloc(&hs->d_slab_ct, sizeof(uint32_t) * std::max<size_t>(sct.size(), 2)));
     COBS_CUDA(cudaMemcpy(hs->d_slab_blocks, sblocks.data(), sizeof(DevBlock) * sblocks.size(),
                          cudaMemcpyHostToDevice));
     COBS_CUDA(cudaMemcpy(hs->d_slab_ct, sct.data(), sizeof(uint32_t) * sct.size(), cudaMemcpyHostToDevice));
     for (int i = 0; i < 2; ++i) {
+        if (file_backed) {
+            COBS_CUDA(cudaHostAlloc(&hs->hstage[i], std::max<uint64_t>(half, 256), cudaHostAllocDefault));
+            COBS_CUDA(cudaEventCreateWithFlags(&hs->h2d_done[i], cudaEventDisableTiming));
+        }
         COBS_CUDA(cudaMalloc(&hs->staging[i], std::max<uint64_t>(half, 256)));
         COBS_CUDA(cudaEventCreateWithFlags(&hs->copied[i], cudaEventDisableTiming));
         COBS_CUDA(cudaEventCreateWithFlags(&hs->consumed[i], cudaEventDisableTiming));
@@ -257,13 +337,13 @@ void upload_rows(DeviceIndex& ix, const ByteSource& src, const std::vector<uint6
 
 } // namespace
 
-std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget) {
+std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget, bool file_backed) {
     auto ix = std::make_unique<DeviceIndex>();
     ix->meta = parse_index(src);
     ix->device = device;
     ix->plan();
     if (hbm_budget > 0 && ix->payload_bytes > hbm_budget) {
-        open_streaming(*ix, src, hbm_budget);
+        open_streaming(*ix, src, hbm_budget, file_backed);
         ix->finish_upload();
         return ix;
     }

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "dev.cuh"
+#include "host.hpp"
 
 namespace cobsg {
 
@@ -74,6 +75,20 @@ struct HostStream {
     uint64_t staging_bytes = 0;
     cudaStream_t copy = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    // File-backed variant: no host copy of the payload; each batch the host
+    // reads every group from the file (threads: pread + repack into the
+    // group's device layout, in a pinned image) and sends it with one DMA.
+    bool file_backed = false;
+    ByteSource src;                              // the index file (file-backed)
+    uint64_t payload_start = 0;                  // file offset of the payload
+    uint8_t* hstage[2] = {nullptr, nullptr};     // pinned group images
+    cudaEvent_t h2d_done[2] = {nullptr, nullptr};
+    bool hstage_busy[2] = {false, false};
+    std::vector<uint64_t> group_bytes;           // staging bytes each group occupies
+    // payload bytes [off, off + len) in file layout, from host memory or the file
+    void read_payload(uint64_t off, void* dst, uint64_t len) const;
+    // file-backed: group gi's slabs, in device-staging layout, into dst
+    void stage_group(const std::vector<DevBlock>& blocks, size_t gi, uint8_t* dst) const;
     ~HostStream();
 };
 
@@ -110,7 +125,8 @@ struct DeviceIndex {
 // Open from a byte source: parse, allocate, stream rows into pitched HBM.
 // With hbm_budget > 0 and a pitched payload larger than it, open in the
 // host-resident streaming mode with two staging buffers of hbm_budget/2.
-std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget = 0);
+std::unique_ptr<DeviceIndex> open_index(const ByteSource& src, int device, uint64_t hbm_budget = 0,
+                                        bool file_backed = false);
 // Blocks [block_lo, block_hi) of a compact index as a standalone compact
 // index resident in HBM (SURVEY.md §8e block sharding): same params, those
 // blocks and their documents; column_offset = the file column of its first

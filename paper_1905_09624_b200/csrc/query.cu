@@ -818,8 +818,20 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
             for (size_t gi = 0; gi < hs.groups.size(); ++gi) {
                 const StreamGroup& G = hs.groups[gi];
                 const int buf = static_cast<int>(gi & 1);
+                if (hs.file_backed) { // host stages the group from the file while the GPU runs the last one
+                    if (hs.hstage_busy[buf]) COBS_CUDA(cudaEventSynchronize(hs.h2d_done[buf]));
+                    hs.stage_group(ix.blocks, gi, hs.hstage[buf]);
+                }
                 COBS_CUDA(cudaStreamWaitEvent(hs.copy, hs.consumed[buf], 0)); // buffer free again
-                for (uint32_t si = G.slab_lo; si < G.slab_hi; ++si) {
+                if (hs.file_backed) {
+                    COBS_CUDA(cudaMemcpyAsync(hs.staging[buf], hs.hstage[buf], hs.group_bytes[gi],
+                                              cudaMemcpyHostToDevice, hs.copy));
+                    COBS_CUDA(cudaEventRecord(hs.h2d_done[buf], hs.copy));
+                    hs.hstage_busy[buf] = true;
+                    for (uint32_t si = G.slab_lo; si < G.slab_hi; ++si)
+                        R.h2d_index_bytes += ix.blocks[hs.slabs[si].block].w * hs.slabs[si].width;
+                }
+                for (uint32_t si = G.slab_lo; si < (hs.file_backed ? G.slab_lo : G.slab_hi); ++si) {
                     const Slab& sl = hs.slabs[si];
                     const DevBlock& d = ix.blocks[sl.block];
                     if (sl.direct)

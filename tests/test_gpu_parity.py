@@ -284,10 +284,13 @@ def _packed(docs):
     return buf, off, doc_segs, names
 
 
-@pytest.mark.parametrize("kind,frac", [(0, 0.9), (1, 1.05), (1, 1.5)])
-def test_host_resident_streaming(gpu, tmp_path, kind, frac):
+@pytest.mark.parametrize("from_file", [False, True], ids=["pinned", "file"])
+@pytest.mark.parametrize("kind,frac", [(0, 0.9), (0, 0.7), (1, 1.05), (1, 1.5)])
+def test_host_resident_streaming(gpu, tmp_path, kind, frac, from_file):
     """Out-of-core mode: with an HBM budget below the pitched payload the index
-    stays in pinned host memory and batches stream it through two staging
+    stays in pinned host memory (or, from_file, is read from the file every
+    batch: pread + repack into pinned group images) and batches stream it
+    through two staging
     buffers (slabs of a block's slices, several blocks per group); results are
     identical to the resident index and the oracle; every batch copies the
     whole payload once."""
@@ -306,7 +309,7 @@ def test_host_resident_streaming(gpu, tmp_path, kind, frac):
     biggest = max(res.width(i) * ((res.row_bytes(i) + 31) // 32 * 32) for i in range(res.block_count()))
     budget = int(pitched * frac) if kind == 0 else int(2 * biggest * frac) + 4096
     budget = min(budget, pitched - 256)
-    st = cb.open_random_access(path, budget, gpu)
+    st = cb.open_random_access(path, budget, gpu, from_file=from_file)
     assert st.streaming() and not res.streaming()
     qb, qo = synth.queries(cfg)
     a = cb.query_batch_raw(res, qb, qo, 1e-12, scores=True)

@@ -26,6 +26,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--budget-gb", type=float, default=8.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "stream.json"))
+    ap.add_argument("--file-dir", default="/tmp", help="where the file-backed leg writes the index")
     a = ap.parse_args()
     cfg = synth.CONFIGS["c3"]
     lengths = synth.doc_lengths(cfg)
@@ -61,6 +62,28 @@ def main():
            "resident_ms_batch": resident.ms_total,
            "resident_qgrams_per_s": grams / (resident.ms_total / 1e3),
            "hits_equal_resident": bool(same), "launches": r.launches}
+    st.close()
+    # file-backed leg: the payload is read from the index file every batch
+    path = os.path.join(a.file_dir, "cobs_stream_bench.cobs")
+    try:
+        with open(path, "wb") as f:
+            f.write(img)
+        del img
+        fb = cb.open_random_access(path, int(a.budget_gb * 2**30), from_file=True)
+        cb.query_batch_raw(fb, qb, qo, cfg.K)  # warm-up (and page cache)
+        runs = [cb.query_batch_raw(fb, qb, qo, cfg.K) for _ in range(3)]
+        f = min(runs, key=lambda x: x.ms_total)
+        out["file_backed"] = {
+            "ms_batch": f.ms_total, "qgrams_per_s": grams / (f.ms_total / 1e3),
+            "index_gbs": f.h2d_index_bytes / (f.ms_total / 1e3) / 1e9,
+            "hits_equal_resident": bool(all(np.array_equal(resident.hits(i)[0], f.hits(i)[0])
+                                            for i in range(len(qo) - 1))),
+            "what": "payload read from the file (page cache) each batch by host threads, repacked "
+                    "into pinned group images, one DMA per group"}
+        fb.close()
+    finally:
+        if os.path.exists(path):
+            os.remove(path)
     print(json.dumps(out))
     json.dump(out, open(a.out, "w"), indent=1)
 
