@@ -154,12 +154,15 @@ inline std::unique_ptr<GpuIndexView> open_resident(const std::string& path, int 
     return std::make_unique<GpuIndexView>(h);
 }
 
-// storage.hpp:23 — for indexes larger than HBM: host-resident, streamed.
+// storage.hpp:23 — for indexes larger than HBM: streamed per batch from
+// pinned host memory, or (from_file) read from the file every batch.
 inline std::unique_ptr<GpuIndexView> open_random_access(const std::string& path, uint64_t hbm_budget,
-                                                        int device = 0) {
+                                                        int device = 0, bool from_file = false) {
     char err[1024];
     cobs_gpu_index* h = nullptr;
-    detail::check(cobs_gpu_index_open_ex(path.c_str(), device, hbm_budget, &h, err, sizeof err), err);
+    detail::check(from_file ? cobs_gpu_index_open_file(path.c_str(), device, hbm_budget, &h, err, sizeof err)
+                            : cobs_gpu_index_open_ex(path.c_str(), device, hbm_budget, &h, err, sizeof err),
+                  err);
     return std::make_unique<GpuIndexView>(h);
 }
 

@@ -138,13 +138,17 @@ inline std::unique_ptr<DeviceIndexView> open_resident(const std::string& path, i
     return std::make_unique<DeviceIndexView>(h);
 }
 
-//! storage.hpp:23 -- an index larger than the HBM budget stays in pinned host
-//! memory and is streamed through HBM per batch.
+//! storage.hpp:23 -- an index larger than the HBM budget is streamed through
+//! HBM per batch, read from the file every batch like the reference's
+//! RandomAccessView (storage.cpp:320-341), or with from_file = false kept in
+//! pinned host memory.
 inline std::unique_ptr<DeviceIndexView> open_random_access(const std::string& path, uint64_t hbm_budget,
-                                                           int device = 0) {
+                                                           int device = 0, bool from_file = true) {
     char err[1024];
     cobs_gpu_index* h = nullptr;
-    check(cobs_gpu_index_open_ex(path.c_str(), device, hbm_budget, &h, err, sizeof err), err);
+    check(from_file ? cobs_gpu_index_open_file(path.c_str(), device, hbm_budget, &h, err, sizeof err)
+                    : cobs_gpu_index_open_ex(path.c_str(), device, hbm_budget, &h, err, sizeof err),
+          err);
     return std::make_unique<DeviceIndexView>(h);
 }
 
