@@ -290,6 +290,9 @@ def ref():
                                       C.c_double, C.c_int, _u64, C.c_int, _u64, C.c_uint32,
                                       C.c_char_p, C.c_char_p, C.c_size_t]
         L.ref_build_terms_write.argtypes = L.ref_build_write.argtypes
+        L.ref_open_random_access.argtypes = [C.c_char_p, C.POINTER(_vp), C.c_char_p, C.c_size_t]
+        L.ref_bytes_read.argtypes = [_vp]
+        L.ref_bytes_read.restype = _u64
         L.ref_open.argtypes = [C.c_char_p, C.POINTER(_vp), C.c_char_p, C.c_size_t]
         L.ref_query_fasta_tsv.argtypes = [_vp, C.c_char_p, C.c_double, _u64, C.POINTER(_vp),
                                           C.c_char_p, C.c_size_t]
@@ -322,13 +325,20 @@ class RefIndex:
         self.h = h
 
     @classmethod
-    def open(cls, path: str) -> "RefIndex":
+    def open(cls, path: str, random_access: bool = False) -> "RefIndex":
+        """open_resident, or open_random_access (rows pread on demand,
+        counted by bytes_read())."""
         h = C.c_void_p()
         err = C.create_string_buffer(1024)
-        rc = ref().ref_open(path.encode(), C.byref(h), err, 1024)
+        fn = ref().ref_open_random_access if random_access else ref().ref_open
+        rc = fn(path.encode(), C.byref(h), err, 1024)
         if rc:
             raise OracleError(rc, err.value.decode())
         return cls(h)
+
+    def bytes_read(self) -> int:
+        """IndexView::bytes_read (index_view.hpp:44-46, storage.cpp:325-336)."""
+        return int(ref().ref_bytes_read(self.h))
 
     @classmethod
     def c5(cls, seed, n_docs, block_size, median, sigma, p, materialise=False, threads=0):

@@ -298,6 +298,19 @@ int ref_open(const char* path, void** out, char* err, size_t errlen) {
     });
 }
 
+// cobs::open_random_access (storage.cpp:320-341): rows pread on demand,
+// bytes_read() counts them (the reference's own traffic accounting).
+int ref_open_random_access(const char* path, void** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<Handle>();
+        h->view = cobs::open_random_access(path);
+        index_names(h.get());
+        *out = h.release();
+    });
+}
+
+uint64_t ref_bytes_read(void* h) { return static_cast<Handle*>(h)->view->bytes_read(); }
+
 int ref_c5_open(uint64_t seed, uint64_t n, uint64_t B, double median, double sigma, double p,
                 int materialise, int threads, void** out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {

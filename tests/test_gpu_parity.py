@@ -599,3 +599,29 @@ def test_sub_batches_equal_one_batch(gpu):
         a, b = one.hits(i), split.hits(i)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     view.close()
+
+
+def test_row_bytes_equal_reference_bytes_read(gpu, tmp_path):
+    """The roofline's algorithmic bytes are the reference's own traffic
+    accounting: the batch's row_bytes (k * sum(l) * sum_b row_bytes_b) equals
+    the bytes the reference's random-access reader fetches for the same
+    queries (bytes_read, storage.cpp:325-336; test_storage.cpp:157-190)."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = random.Random(66)
+    docs = [(b"b%03d" % i, [rand(rng, rng.randrange(100, 4000))]) for i in range(150)]
+    path = str(tmp_path / "ra.cobs")
+    for k, kind in ((1, cb.KIND_COMPACT), (3, cb.KIND_COMPACT), (2, cb.KIND_CLASSIC)):
+        params = cb.IndexParams(k=k, block_size=40)
+        cb.build_image(docs, params, kind, path=path, device=gpu)
+        view = cb.open_resident(path, gpu)
+        pats = [docs[rng.randrange(150)][1][0][:rng.randrange(31, 600)] for _ in range(25)] + [b"ACG"]
+        ra = O.RefIndex.open(path, random_access=True)
+        for p in pats:
+            try:
+                ra.query(p, 0.5)
+            except O.OracleError:
+                pass
+        got = cb.query_batch(view, pats, 0.5)
+        assert got.row_bytes == ra.bytes_read(), (k, kind)
+        view.close()
