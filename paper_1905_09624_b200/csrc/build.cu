@@ -670,6 +670,8 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
 
     Event e0, e1, e2, e3;
 
+    NvtxPhase phase;
+    phase.begin("cobs.build.count");
     // ---- count pass, in waves of documents whose sets fit in L2 ---------
     // (random CAS into L2-resident sets instead of DRAM; a document larger
     // than a wave gets a wave of its own)
@@ -893,6 +895,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
     }
 
+    phase.begin("cobs.build.sizing");
     // ---- host: order, blocks, widths ------------------------------------
     IndexMeta meta;
     meta.params = P;
@@ -923,6 +926,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     meta.layout();
     (void)meta.header_bytes(); // DataError for names longer than 65,535 bytes (storage.cpp:368)
 
+    phase.begin("cobs.build.fill");
     // ---- fill pass, straight into the pitched HBM layout of a DeviceIndex
     auto ix = std::make_unique<DeviceIndex>();
     ix->meta = std::move(meta);

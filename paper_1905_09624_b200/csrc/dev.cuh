@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "host.hpp"
 
@@ -17,6 +18,22 @@ namespace cobsg {
     } while (0)
 
 // RAII CUDA event (destroyed on every exit path).
+// NVTX phase ranges (header-only NVTX3; free unless a profiler attaches):
+// begin() closes the previous phase, the destructor the last one.
+struct NvtxPhase {
+    bool on = false;
+    void begin(const char* name) {
+        end();
+        nvtxRangePushA(name);
+        on = true;
+    }
+    void end() {
+        if (on) nvtxRangePop();
+        on = false;
+    }
+    ~NvtxPhase() { end(); }
+};
+
 struct Event {
     cudaEvent_t e = nullptr;
     explicit Event(unsigned flags = cudaEventDefault) {

@@ -717,6 +717,8 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     Event ev[4];
     COBS_CUDA(cudaEventRecord(ev[0], st));
 
+    NvtxPhase phase;
+    phase.begin("cobs.query.termize");
     // kernel 1
     TermizeArgs ta{};
     ta.pats = d_pats;
@@ -751,6 +753,7 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     R.launches += 1;
     COBS_CUDA(cudaEventRecord(ev[1], st));
 
+    phase.begin("cobs.query.gather");
     // kernel 2
     const bool want_scores = flags & COBS_Q_SCORES;
     const bool want_hits = (flags & COBS_Q_HITS) || !(flags & COBS_Q_SCORES);
@@ -870,6 +873,7 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         ws.hit_score.reserve(4 * ws.hit_cap);
     }
 
+    phase.begin("cobs.query.order");
     // kernel 3: order hits by (query, score desc, name asc)
     const uint64_t m = h_total;
     if (want_hits && m > 0) {
