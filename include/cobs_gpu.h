@@ -205,7 +205,8 @@ void cobs_gpu_results_free(cobs_gpu_results* r);
  * storage.hpp:14-16).  Content strings i are bytes [seg_offsets[i],
  * seg_offsets[i+1]) of `seqs`; document d owns strings
  * [doc_segs[d], doc_segs[d+1]) (grams never span strings); names[d] is a
- * NUL-terminated name.  kind: COBS_KIND_CLASSIC (documents in input order,
+ * NUL-terminated name (so build names cannot contain NUL bytes; the reader
+ * accepts any name bytes the format allows).  kind: COBS_KIND_CLASSIC (documents in input order,
  * width forced_w or sized for the largest document) or COBS_KIND_COMPACT
  * (sorted by (term_count, name), blocks of block_size).  The image written
  * to `out_path` (if non-NULL) and/or returned through `image`/`image_len`

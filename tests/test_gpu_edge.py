@@ -104,3 +104,27 @@ def test_forced_tag_collisions_stay_exact(gpu):
             check(img, pats, Ks=(1e-12, 0.5), tops=(0,))
     finally:
         del os.environ["COBS_DEBUG_TAG_BITS"]
+
+
+def test_tie_order_with_non_ascii_names(gpu, tmp_path):
+    """Hit order (score desc, name asc) compares names as unsigned bytes
+    (std::string <, query.cpp:156-160): names with bytes >= 0x80, prefixes
+    of one another, all scoring the same -- the device order equals the
+    reference's query() on the same file, with and without top_t.  (Build
+    entry points take NUL-terminated names.)"""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    seq = b"ACGT" * 40 + b"TTGACA" * 20
+    names = [b"\xff", b"\x80a", b"a\x01b", b"a", b"ab", b"A", b"\x7f", b"z\xc3\xa9", b"zz"]
+    docs = [(n, [seq]) for n in names]
+    path = str(tmp_path / "names.cobs")
+    cb.build_compact(docs, cb.IndexParams(block_size=3), path=path, device=gpu)
+    view = cb.open_resident(path, gpu)
+    ref = O.RefIndex.open(path)
+    for top_t in (0, 4):
+        got = cb.query(view, seq[:120], cb.QueryOptions(K=0.5, top_t=top_t))
+        _, _, want = ref.query(seq[:120], 0.5, top_t)
+        all_names = view.doc_names()
+        assert [(h.doc_name, h.score) for h in got.hits] == [(all_names[d], s) for d, s in want]
+        assert len({h.score for h in got.hits}) == 1  # a genuine tie
+    view.close()
