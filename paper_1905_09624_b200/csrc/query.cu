@@ -8,10 +8,15 @@
 //             slice): stream the k rows of every term (128-byte coalesced
 //             loads), AND them, add the 32-bit document masks into bit-sliced
 //             counters with a carry-save (Harley-Seal) adder, then threshold
-//             and compact hits; optional dense scores.
+//             and compact hits; optional dense scores.  Small batches split
+//             one query's terms over a CTA's 8 warps (counts added
+//             bit-sliced); an index streamed from host memory or the file
+//             is gathered slab group by slab group.
 //                                      (reference: query.cpp:49-119)
 //   kernel 3  ordering              CUB radix sorts on (query, score desc,
 //             name rank asc) (reference: query.cpp:156-162).
+// A host batch too large for the free HBM runs as sub-batches (results
+// concatenated, one dense score width).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
