@@ -166,6 +166,18 @@ inline std::unique_ptr<GpuIndexView> open_random_access(const std::string& path,
     return std::make_unique<GpuIndexView>(h);
 }
 
+// Block sharding: blocks [block_lo, block_hi) of a compact
+// index as a standalone compact index; column_offset() maps its columns to
+// the file's.  Merge shard hit lists by (score desc, name asc), cut to top_t.
+inline std::unique_ptr<GpuIndexView> open_blocks(const std::string& path, uint64_t block_lo, uint64_t block_hi,
+                                                 int device = 0) {
+    char err[1024];
+    cobs_gpu_index* h = nullptr;
+    detail::check(cobs_gpu_index_open_blocks(path.c_str(), device, block_lo, block_hi, &h, err, sizeof err), err);
+    return std::make_unique<GpuIndexView>(h);
+}
+inline uint64_t column_offset(const GpuIndexView& v) { return cobs_gpu_index_column_offset(v.handle()); }
+
 // storage.hpp:14 — byte-identical to the reference writer.
 inline void write_index(const GpuIndexView& index, const std::string& path) {
     char err[1024];

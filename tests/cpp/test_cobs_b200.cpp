@@ -3,6 +3,7 @@
 // test_storage.cpp, test_index.cpp) and checked against the CPU oracle
 // (oracle/cobs_oracle.h, test infrastructure) and the reference's golden
 // vectors.  Build: `make cpptest`; run: tests/cpp/test_cobs_b200.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -303,6 +304,65 @@ TEST_CASE(device_build_equals_the_oracle_build) { // byte-identical files
             orc_free(img);
         }
     }
+}
+
+TEST_CASE(block_shards_merge_to_the_whole_index) {
+    std::mt19937_64 rng(2024);
+    auto docs = gen_docs(rng, 50, 200, 4000);
+    IndexParams p;
+    p.block_size = 6;
+    auto built = build_compact(docs, p);
+    write_index(*built, tmp_path("s.cobs"));
+    auto whole = open_resident(tmp_path("s.cobs"));
+    const uint64_t nb = whole->block_count();
+    auto s0 = open_blocks(tmp_path("s.cobs"), 0, nb / 2);
+    auto s1 = open_blocks(tmp_path("s.cobs"), nb / 2, nb);
+    CHECK(column_offset(*s0) == 0 && column_offset(*s1) == s0->total_docs());
+    std::vector<std::string> pats;
+    for (int i = 0; i < 8; ++i) pats.push_back(docs[(i * 7) % docs.size()].content[0].substr(0, 300));
+    for (uint64_t top_t : {uint64_t(0), uint64_t(3)}) {
+        QueryOptions o;
+        o.K = 0.3;
+        o.top_t = top_t;
+        auto w = query_batch(*whole, pats, o, nullptr);
+        auto a = query_batch(*s0, pats, o, nullptr);
+        auto b = query_batch(*s1, pats, o, nullptr);
+        for (size_t i = 0; i < pats.size(); ++i) {
+            std::vector<ScoredHit> m = a[i].hits;
+            m.insert(m.end(), b[i].hits.begin(), b[i].hits.end());
+            std::sort(m.begin(), m.end(), [](const ScoredHit& x, const ScoredHit& y) {
+                return x.score != y.score ? x.score > y.score : x.doc_name < y.doc_name;
+            });
+            if (top_t && m.size() > top_t) m.resize(top_t);
+            CHECK(m == w[i].hits);
+            CHECK(a[i].ell == w[i].ell && b[i].ell == w[i].ell);
+        }
+    }
+    CHECK_THROWS_AS(open_blocks(tmp_path("s.cobs"), 1, 1), std::invalid_argument);
+}
+
+TEST_CASE(file_backed_streaming_equals_resident) { // storage.hpp:23 from the file
+    std::mt19937_64 rng(77);
+    auto docs = gen_docs(rng, 40, 500, 6000);
+    IndexParams p;
+    p.block_size = 5;
+    auto built = build_compact(docs, p);
+    write_index(*built, tmp_path("f.cobs"));
+    auto res = open_resident(tmp_path("f.cobs"));
+    uint64_t biggest = 0;
+    for (size_t b = 0; b < res->block_count(); ++b)
+        biggest = std::max<uint64_t>(biggest, res->width(b) * ((res->row_bytes(b) + 31) / 32 * 32));
+    auto fb = open_random_access(tmp_path("f.cobs"), 2 * biggest + 4096, 0, /*from_file=*/true);
+    CHECK(fb->streaming() && !res->streaming());
+    std::vector<std::string> pats;
+    for (int i = 0; i < 6; ++i) pats.push_back(docs[i * 5].content[0].substr(100, 400));
+    QueryOptions o;
+    o.K = 0.4;
+    auto x = query_batch(*res, pats, o, nullptr);
+    auto y = query_batch(*fb, pats, o, nullptr);
+    for (size_t i = 0; i < pats.size(); ++i) CHECK(x[i].hits == y[i].hits && x[i].ell == y[i].ell);
+    write_index(*fb, tmp_path("f2.cobs"));
+    CHECK(read_file(tmp_path("f.cobs")) == read_file(tmp_path("f2.cobs")));
 }
 
 int main() {
