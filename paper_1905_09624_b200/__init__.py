@@ -121,6 +121,7 @@ class BatchResult:
     launches: int
     row_bytes: int
     h2d_index_bytes: int = 0
+    gather_path: int = 0  # 0 gather_kernel, 1 L2-tiled gather
 
     def hits(self, i: int) -> Tuple[np.ndarray, np.ndarray]:
         o, n = int(self.hit_off[i]), int(self.hit_n[i])
@@ -377,7 +378,8 @@ def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: 
             dense=dense, ms_termize=t[0].value, ms_gather=t[1].value, ms_order=t[2].value,
             ms_total=t[3].value, launches=int(N.lib.cobs_gpu_results_launches(r)),
             row_bytes=int(N.lib.cobs_gpu_results_row_bytes(r)),
-            h2d_index_bytes=int(N.lib.cobs_gpu_results_h2d_index_bytes(r)))
+            h2d_index_bytes=int(N.lib.cobs_gpu_results_h2d_index_bytes(r)),
+            gather_path=int(N.lib.cobs_gpu_results_gather_path(r)))
     finally:
         N.lib.cobs_gpu_results_free(r)
 

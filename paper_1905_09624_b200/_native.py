@@ -83,6 +83,7 @@ SIGNATURES = {
                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "cobs_gpu_results_launches": (C.c_uint32, [vp]),
     "cobs_gpu_results_row_bytes": (C.c_uint64, [vp]),
+    "cobs_gpu_results_gather_path": (C.c_uint32, [vp]),
     "cobs_gpu_results_h2d_index_bytes": (C.c_uint64, [vp]),
     "cobs_gpu_results_free": (None, [vp]),
     "cobs_gpu_build": (C.c_int, [vp, vp, C.c_uint64, vp, C.POINTER(C.c_char_p), C.c_uint64,

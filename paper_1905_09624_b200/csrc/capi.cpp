@@ -323,6 +323,8 @@ uint32_t cobs_gpu_results_launches(const cobs_gpu_results* r) { return r->r.laun
 
 uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r) { return r->r.row_bytes; }
 
+uint32_t cobs_gpu_results_gather_path(const cobs_gpu_results* r) { return r->r.tiled ? 1u : 0u; }
+
 uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r) { return r->r.h2d_index_bytes; }
 
 void cobs_gpu_results_free(cobs_gpu_results* r) { delete r; }

@@ -44,6 +44,7 @@ struct QueryWorkspace {
     DevBuf hit_count, hit_total, hit_q, hit_doc, hit_score;
     DevBuf key64, key64_alt, key32, key32_alt, perm, perm_alt, out_doc, out_score;
     DevBuf scores, cub_tmp;
+    DevBuf tlist, tdone, tshift; // L2-tiled gather (tiled.cu): bucketed row lists, phase counters, range shifts
     PinnedBuf h_small;
     uint64_t hit_cap = 0;
 };
@@ -149,6 +150,7 @@ struct QueryResults {
     uint32_t score_bytes = 2;
     double ms_termize = 0, ms_gather = 0, ms_order = 0, ms_total = 0;
     uint32_t launches = 0; // kernels of ours launched by the batch
+    bool tiled = false;    // kernel 2 ran as the L2-tiled gather (tiled.cu)
     uint64_t h2d_index_bytes = 0; // streaming mode: payload bytes copied to HBM
     uint64_t row_bytes = 0;
 };

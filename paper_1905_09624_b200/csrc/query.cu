@@ -24,7 +24,9 @@
 #include <type_traits>
 
 #include "../../include/cobs_gpu.h"
+#include "gather_common.cuh"
 #include "index.hpp"
+#include "tiled.hpp"
 
 namespace cobsg {
 
@@ -272,92 +274,6 @@ struct GatherArgs {
     uint32_t* hit_doc;
     uint32_t* hit_score;
 };
-
-// Carry-save adder: (hi, lo) = a + b + c.
-__device__ __forceinline__ void csa(uint32_t& hi, uint32_t& lo, uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t u = a ^ b;
-    hi = (a & b) | (u & c);
-    lo = u ^ c;
-}
-
-template <bool EF>
-__device__ __forceinline__ uint32_t ld_row(const uint8_t* p, uint64_t policy) {
-    uint32_t v;
-    if (EF)
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
-            : "=r"(v)
-            : "l"(p), "l"(policy));
-    else
-        asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
-// rowbase + row * pitch in one IMAD.WIDE.U32.
-__device__ __forceinline__ const uint8_t* row_addr(const uint8_t* base, uint32_t row, uint32_t pitch) {
-    const uint8_t* p;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(row), "r"(pitch), "l"(base));
-    return p;
-}
-
-// Bit-sliced counters: a document's count is sum_p 2^p * bit(F[p]).
-template <int NT>
-__device__ __forceinline__ void add_at(uint32_t (&F)[NT], int level, uint32_t x) {
-#pragma unroll
-    for (int p = 0; p < NT; ++p) {
-        if (p >= level) {
-            uint32_t t = F[p] & x;
-            F[p] ^= x;
-            x = t;
-        }
-    }
-}
-
-template <int NT>
-__device__ __forceinline__ uint32_t extract(const uint32_t (&F)[NT], int i) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int p = 0; p < NT; ++p) s |= ((F[p] >> i) & 1u) << p;
-    return s;
-}
-
-// Bit-sliced F >= T over the 32 documents of a lane at once.
-template <int NT>
-__device__ __forceinline__ uint32_t ge_mask(const uint32_t (&F)[NT], uint32_t T) {
-    uint32_t gt = 0, eq = 0xffffffffu;
-#pragma unroll
-    for (int p = NT - 1; p >= 0; --p) {
-        const uint32_t tb = ((T >> p) & 1u) ? 0xffffffffu : 0u;
-        gt |= eq & F[p] & ~tb;
-        eq &= ~(F[p] ^ tb);
-    }
-    if constexpr (NT < 32) {
-        if ((T >> NT) != 0u) return 0u; // T beyond the representable counts
-    }
-    return gt | eq;
-}
-
-// Harley-Seal step: 16 document masks into the carry-save accumulators;
-// returns the weight-16 carry.
-__device__ __forceinline__ uint32_t csa16(const uint32_t* v, uint32_t& ones, uint32_t& twos,
-                                          uint32_t& fours, uint32_t& eights) {
-    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
-    csa(twosA, ones, ones, v[0], v[1]);
-    csa(twosB, ones, ones, v[2], v[3]);
-    csa(foursA, twos, twos, twosA, twosB);
-    csa(twosA, ones, ones, v[4], v[5]);
-    csa(twosB, ones, ones, v[6], v[7]);
-    csa(foursB, twos, twos, twosA, twosB);
-    csa(eightsA, fours, fours, foursA, foursB);
-    csa(twosA, ones, ones, v[8], v[9]);
-    csa(twosB, ones, ones, v[10], v[11]);
-    csa(foursA, twos, twos, twosA, twosB);
-    csa(twosA, ones, ones, v[12], v[13]);
-    csa(twosB, ones, ones, v[14], v[15]);
-    csa(foursB, twos, twos, twosA, twosB);
-    csa(eightsB, fours, fours, foursA, foursB);
-    csa(sixteens, eights, eights, eightsA, eightsB);
-    return sixteens;
-}
 
 // One warp = one (query, column task): 32 lanes x 4 bytes = the 128-byte,
 // 1024-document slice of every addressed row.  Per chunk of CH terms the
@@ -797,7 +713,9 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     ga.hit_total = ws.hit_total.as<unsigned long long>();
     bool w32 = true;
     for (const DevBlock& d : ix.blocks) w32 &= d.w <= 0xffffffffull;
-    GatherFn fn = pick_gather(nt_needed, (w32 && k <= 3) ? static_cast<int>(k) : 0, ix.evict_first);
+    bool ef = ix.evict_first;
+    if (const char* e = std::getenv("COBS_EF")) ef = std::atoi(e) != 0; // A/B of the L2 policy
+    GatherFn fn = pick_gather(nt_needed, (w32 && k <= 3) ? static_cast<int>(k) : 0, ef);
     // Term split for batches too small to fill the GPU with one warp per
     // (query, column task): fewer than ~4 resident waves of warps.
     ga.split = static_cast<uint64_t>(n) * ga.nct < 4ull * 148 * 24 ? 8 : 1;
@@ -807,6 +725,8 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     const uint64_t tiles = (n + qt - 1) / qt;
     const uint64_t grid2 = tiles * ((qt + qpc - 1) / qpc) * ga.nct;
     if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
+    const TiledPlan tp = ix.streaming() ? TiledPlan() : tiled_plan(ix, win_base, n, nt_needed, ga.prune != 0);
+    R.tiled = tp.use;
     unsigned long long h_total = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         ga.hit_cap = ws.hit_cap;
@@ -817,7 +737,23 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         COBS_CUDA(cudaMemsetAsync(ws.hit_total.ptr, 0, 8, st));
         if (attempt == 0) COBS_CUDA(cudaEventRecord(ev[1], st));
         if (!ix.streaming()) {
-            if (grid2 > 0) {
+            if (tp.use) { // L2-tiled gather (tiled.cu)
+                TiledIO io{};
+                io.hashes = ga.hashes;
+                io.win_base = ga.win_base;
+                io.ell = ga.ell;
+                io.tau = ga.tau;
+                io.D = D;
+                io.scores = ga.scores;
+                io.want_hits = ga.want_hits;
+                io.hit_count = ga.hit_count;
+                io.hit_total = ga.hit_total;
+                io.hit_cap = ga.hit_cap;
+                io.hit_q = ga.hit_q;
+                io.hit_doc = ga.hit_doc;
+                io.hit_score = ga.hit_score;
+                R.launches += tiled_gather(ix, tp, st, io);
+            } else if (grid2 > 0) {
                 fn<<<static_cast<unsigned>(grid2), 256, split_smem, st>>>(ga);
                 R.launches += 1;
             }
