@@ -472,7 +472,10 @@ TiledPlan tiled_plan(DeviceIndex& ix, const std::vector<uint64_t>& win_base, uin
     TiledPlan tp;
     const char* env = std::getenv("COBS_TILED");
     const int mode = env ? std::atoi(env) : -1; // 0 off, 1 force (when eligible), -1 auto
-    if (mode == 0) return tp.why = "off", tp;
+    // Measured slower than gather_kernel on every shape tried (DESIGN.md
+    // section 2, "L2-tiled gather"): opt-in only, auto never selects it --
+    // and returns before any CUDA query, so the default batch pays nothing.
+    if (mode != 1) return tp.why = mode == 0 ? "off" : "auto: the warp-per-query gather is faster", tp;
     const Params& P = ix.meta.params;
     if (ix.streaming()) return tp.why = "streaming index", tp;
     if (P.k != 1) return tp.why = "k > 1", tp;
@@ -515,10 +518,7 @@ TiledPlan tiled_plan(DeviceIndex& ix, const std::vector<uint64_t>& win_base, uin
     // index is far larger than L2 (a small index is L2-resident anyway)
     const double reuse = static_cast<double>(std::min<uint64_t>(per_wave, n)) * avg_w /
                          (static_cast<double>(sum_w) / std::max<uint64_t>(nb, 1));
-    // Measured slower than gather_kernel on every shape tried (DESIGN.md
-    // section 2, "L2-tiled gather"): opt-in only, auto never selects it.
-    (void)reuse;
-    if (mode < 0) return tp.why = "auto: the warp-per-query gather is faster", tp;
+    (void)reuse; // (a future auto mode would require reuse >= 2 and an index far larger than L2)
     tp.qs = static_cast<uint32_t>(qs);
     tp.grid = static_cast<uint32_t>(nsm);
     for (uint64_t q0 = 0; q0 < n; q0 += per_wave) {

@@ -1,5 +1,5 @@
 #!/bin/bash
-# End-of-round-1 captures with the final code: the bench launch list (ncu
+# End-of-round captures with the final code: the bench launch list (ncu
 # gpu__time_duration, cold, serialised) and one --set full capture each of
 # the gather and termize kernels on a 10k-document C5 instance (15 GB, so
 # ncu's replay save/restore fits).  Each command first runs without ncu.
