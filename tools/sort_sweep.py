@@ -1,5 +1,7 @@
-# A/B of the bin-sorted gather (COBS_SORT / COBS_SORT_TSHIFT) on one C5-shaped
-# index in one process (tools only).  usage: sort_sweep.py [docs] [queries]
+# A/B of a bin-sorted, clock-rotated gather_kernel variant (COBS_SORT /
+# COBS_SORT_MODE / COBS_SORT_TSHIFT) on one C5-shaped index (tools only).  The
+# variant was measured slower and removed ("HBM page locality");
+# this script documents the A/B.  usage: sort_sweep.py [docs] [queries]
 import json, os, sys
 sys.path.insert(0, '.')
 import paper_1905_09624_b200 as cb
