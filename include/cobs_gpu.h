@@ -255,6 +255,11 @@ int cobs_gpu_merge_classic(const cobs_gpu_index* a, const cobs_gpu_index* b, int
  * counting, fill (sequences in HBM -> finished matrix), total incl. H2D,
  * D2H and serialisation. */
 int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total);
+/* The same plus the host<->device copy legs of the last build: sequences
+ * H2D (0 when they were already on the device) and the index image D2H
+ * (0 when the index stayed in HBM). */
+int cobs_gpu_build_timing_ex(double* ms_h2d, double* ms_count, double* ms_fill, double* ms_d2h,
+                             double* ms_total);
 
 void cobs_gpu_free(void* p);
 

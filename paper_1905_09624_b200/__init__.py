@@ -584,3 +584,10 @@ def last_build_timing() -> Tuple[float, float, float]:
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     N.lib.cobs_gpu_build_timing(C.byref(a), C.byref(b), C.byref(c))
     return a.value, b.value, c.value
+
+
+def last_build_timing_ex() -> dict:
+    """ms of the last build's legs: h2d, count, fill, d2h, total."""
+    v = [C.c_double() for _ in range(5)]
+    N.lib.cobs_gpu_build_timing_ex(*(C.byref(x) for x in v))
+    return dict(zip(("ms_h2d", "ms_count", "ms_fill", "ms_d2h", "ms_total"), (x.value for x in v)))

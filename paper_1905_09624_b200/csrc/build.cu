@@ -646,8 +646,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     d_docstart.reserve(8 * n_docs);
     d_tc.reserve(8 * n_docs);
     auto t_h2d = std::chrono::steady_clock::now();
-    if (!seqs_on_device)
-        COBS_CUDA(cudaMemcpyAsync(d_seqs.ptr, seqs, total_bytes, cudaMemcpyHostToDevice, st));
+    if (!seqs_on_device) h2d_staged(d_seqs.ptr, seqs, total_bytes, st);
     COBS_CUDA(cudaMemcpyAsync(d_segoff.ptr, seg_off, 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_rbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     if (n_segs)
@@ -1054,24 +1053,35 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     return ix;
 }
 
-std::vector<uint8_t> index_image(const DeviceIndex& ix) {
-    std::vector<uint8_t> header = ix.meta.header_bytes();
+uint64_t index_image_size(const DeviceIndex& ix) {
+    return ix.meta.header_bytes().size() + (ix.meta.file_size - ix.meta.payload_start);
+}
+
+void index_image_into(const DeviceIndex& ix, uint8_t* dst) {
+    const std::vector<uint8_t> header = ix.meta.header_bytes();
     const uint64_t payload = ix.meta.file_size - ix.meta.payload_start;
-    std::vector<uint8_t> image(header.size() + payload);
-    std::memcpy(image.data(), header.data(), header.size());
+    std::memcpy(dst, header.data(), header.size());
     if (ix.streaming()) { // host-resident: the payload is already in file layout
-        ix.hs->read_payload(0, image.data() + header.size(), payload);
-        return image;
+        ix.hs->read_payload(0, dst + header.size(), payload);
+        return;
     }
     COBS_CUDA(cudaSetDevice(ix.device));
     uint64_t off = header.size();
-    for (const DevBlock& d : ix.blocks) { // un-pitch on the copy engine
-        if (d.w)
-            COBS_CUDA(cudaMemcpy2D(image.data() + off, d.rb, ix.payload + d.base, d.pitch, d.rb, d.w,
-                                   cudaMemcpyDeviceToHost));
+    for (const DevBlock& d : ix.blocks) { // pitched 1D chunks, un-pitched on the host
+        d2h_unpitch(dst + off, ix.payload + d.base, d.w, d.rb, d.pitch, ix.stream);
         off += d.w * d.rb;
     }
+}
+
+std::vector<uint8_t> index_image(const DeviceIndex& ix) {
+    std::vector<uint8_t> image(index_image_size(ix));
+    index_image_into(ix, image.data());
     return image;
+}
+
+void note_image_ms(double ms) {
+    g_timing.ms_d2h = ms;
+    g_timing.ms_total += ms;
 }
 
 std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, uint64_t n_segs,
@@ -1087,9 +1097,13 @@ std::vector<uint8_t> build_index(const uint8_t* seqs, const uint64_t* seg_off, u
 }
 
 void write_image(const std::vector<uint8_t>& image, const std::string& path) {
+    write_image(image.data(), image.size(), path);
+}
+
+void write_image(const uint8_t* image, uint64_t size, const std::string& path) {
     std::ofstream out(path, std::ios::binary | std::ios::trunc); // storage.cpp:382-396
     if (!out) throw DataError("cannot create index file: " + path);
-    out.write(reinterpret_cast<const char*>(image.data()), static_cast<std::streamsize>(image.size()));
+    out.write(reinterpret_cast<const char*>(image), static_cast<std::streamsize>(size));
     out.flush();
     if (!out) throw DataError("error writing index file: " + path);
 }

@@ -33,7 +33,13 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                                                 bool seqs_on_device, bool terms_input = false);
 // File image (header + un-pitched payload) of a device-resident index.
 std::vector<uint8_t> index_image(const DeviceIndex& ix);
+// The same into caller memory of index_image_size() bytes (no zero fill).
+uint64_t index_image_size(const DeviceIndex& ix);
+void index_image_into(const DeviceIndex& ix, uint8_t* dst);
+// Record the image leg of the last build (ms_d2h, added to ms_total).
+void note_image_ms(double ms);
 void write_image(const std::vector<uint8_t>& image, const std::string& path);
+void write_image(const uint8_t* image, uint64_t size, const std::string& path);
 
 void synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo, uint64_t doc_hi,
                 uint8_t* dev_out, int device);

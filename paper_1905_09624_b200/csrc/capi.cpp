@@ -3,6 +3,7 @@
 // (proj/src/cli.cpp:448-454).
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <memory>
 
@@ -343,14 +344,18 @@ int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t
         auto ix = cobsg::build_device_index(seqs, seg_offsets, n_segs, doc_segs, nm, to_params(params),
                                             static_cast<uint8_t>(kind), forced_w, device,
                                             (flags & COBS_B_DEVICE_INPUT) != 0, (flags & COBS_B_TERMS) != 0);
-        if (out_path || image) {
-            std::vector<uint8_t> img = cobsg::index_image(*ix);
-            if (out_path) cobsg::write_image(img, out_path);
+        if (out_path || image) { // the image is made once, straight into the returned buffer
+            const auto t0 = std::chrono::steady_clock::now();
+            const uint64_t size = cobsg::index_image_size(*ix);
+            uint8_t* buf = static_cast<uint8_t*>(std::malloc(std::max<size_t>(size, 1)));
+            if (!buf) throw std::bad_alloc();
+            std::unique_ptr<uint8_t, decltype(&std::free)> hold(buf, &std::free);
+            cobsg::index_image_into(*ix, buf);
+            cobsg::note_image_ms(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            if (out_path) cobsg::write_image(buf, size, out_path);
             if (image) {
-                *image = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
-                if (!*image) throw std::bad_alloc();
-                std::memcpy(*image, img.data(), img.size());
-                *image_len = img.size();
+                *image = hold.release();
+                *image_len = size;
             }
         }
         if (index_out) {
@@ -417,6 +422,17 @@ int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total) {
     const cobsg::BuildTiming& t = cobsg::last_build_timing();
     if (ms_count) *ms_count = t.ms_count;
     if (ms_fill) *ms_fill = t.ms_fill;
+    if (ms_total) *ms_total = t.ms_total;
+    return COBS_OK;
+}
+
+int cobs_gpu_build_timing_ex(double* ms_h2d, double* ms_count, double* ms_fill, double* ms_d2h,
+                             double* ms_total) {
+    const cobsg::BuildTiming& t = cobsg::last_build_timing();
+    if (ms_h2d) *ms_h2d = t.ms_h2d;
+    if (ms_count) *ms_count = t.ms_count;
+    if (ms_fill) *ms_fill = t.ms_fill;
+    if (ms_d2h) *ms_d2h = t.ms_d2h;
     if (ms_total) *ms_total = t.ms_total;
     return COBS_OK;
 }

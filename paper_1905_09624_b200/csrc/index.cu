@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <numeric>
 #include <thread>
 
@@ -39,6 +40,115 @@ void PinnedBuf::reserve(size_t n) {
 }
 PinnedBuf::~PinnedBuf() {
     if (ptr) cudaFreeHost(ptr);
+}
+
+namespace {
+
+// Process-wide pinned staging (two buffers, allocated once: cudaMallocHost of
+// this size costs milliseconds, far more than a copy of it).
+constexpr uint64_t kStageBytes = 64ull << 20;
+struct StagePool {
+    std::mutex mu;
+    PinnedBuf buf[2];
+};
+StagePool& stage_pool() {
+    static StagePool p;
+    return p;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// f(lo, hi) over [0, n) split across up to 8 host threads (small n: inline)
+template <typename F>
+void host_parallel(uint64_t n, uint64_t grain, F&& f) {
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const uint64_t parts = std::min<uint64_t>(hw, (n + grain - 1) / std::max<uint64_t>(grain, 1));
+    if (parts <= 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const uint64_t per = (n + parts - 1) / parts;
+    for (uint64_t i = 1; i < parts; ++i)
+        th.emplace_back([&, i] { f(std::min(n, i * per), std::min(n, (i + 1) * per)); });
+    f(0, std::min(n, per));
+    for (auto& t : th) t.join();
+}
+
+} // namespace
+
+void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (bytes <= (4ull << 20) || is_pinned(src_host)) {
+        COBS_CUDA(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    StagePool& P = stage_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+    bool busy[2] = {false, false};
+    const uint8_t* src = static_cast<const uint8_t*>(src_host);
+    uint8_t* dst = static_cast<uint8_t*>(dst_dev);
+    for (uint64_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
+        const int b = static_cast<int>(i & 1);
+        const uint64_t len = std::min(kStageBytes, bytes - off);
+        P.buf[b].reserve(kStageBytes);
+        if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // its last DMA has drained
+        uint8_t* stage = P.buf[b].as<uint8_t>();
+        host_parallel(len, 8ull << 20, [&](uint64_t lo, uint64_t hi) { std::memcpy(stage + lo, src + off + lo, hi - lo); });
+        COBS_CUDA(cudaMemcpyAsync(dst + off, stage, len, cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaEventRecord(done[b], st));
+        busy[b] = true;
+    }
+    for (int b = 0; b < 2; ++b)
+        if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // the pool is reused after return
+}
+
+void d2h_unpitch(void* dst_host, const uint8_t* src_dev, uint64_t rows, uint32_t row_bytes, uint32_t pitch,
+                 cudaStream_t st) {
+    if (rows == 0 || row_bytes == 0) return;
+    uint8_t* dst = static_cast<uint8_t*>(dst_host);
+    const uint64_t chunk_rows = std::max<uint64_t>(1, kStageBytes / pitch);
+    if (pitch == row_bytes && is_pinned(dst_host)) {
+        COBS_CUDA(cudaMemcpyAsync(dst, src_dev, rows * pitch, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    StagePool& P = stage_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+    const uint64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
+    auto issue = [&](uint64_t c) {
+        const int b = static_cast<int>(c & 1);
+        const uint64_t r0 = c * chunk_rows, n = std::min(chunk_rows, rows - r0);
+        P.buf[b].reserve(kStageBytes);
+        COBS_CUDA(cudaMemcpyAsync(P.buf[b].ptr, src_dev + r0 * pitch, n * pitch, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaEventRecord(done[b], st));
+    };
+    issue(0);
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int b = static_cast<int>(c & 1);
+        COBS_CUDA(cudaEventSynchronize(done[b]));
+        if (c + 1 < nchunks) issue(c + 1); // the next chunk's DMA runs while this one is unpacked
+        const uint64_t r0 = c * chunk_rows, n = std::min(chunk_rows, rows - r0);
+        const uint8_t* stage = P.buf[b].as<uint8_t>();
+        if (pitch == row_bytes)
+            host_parallel(n * pitch, 8ull << 20, [&](uint64_t lo, uint64_t hi) {
+                std::memcpy(dst + r0 * row_bytes + lo, stage + lo, hi - lo);
+            });
+        else
+            host_parallel(n, (8ull << 20) / pitch + 1, [&](uint64_t lo, uint64_t hi) {
+                for (uint64_t r = lo; r < hi; ++r)
+                    std::memcpy(dst + (r0 + r) * row_bytes, stage + r * pitch, row_bytes);
+            });
+    }
 }
 
 DeviceIndex::~DeviceIndex() {

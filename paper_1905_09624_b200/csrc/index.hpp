@@ -123,6 +123,18 @@ struct DeviceIndex {
     void finish_upload(); // block table, tasks, ranks -> HBM
 };
 
+// Host <-> device copies of large pageable host buffers through a cached
+// pair of pinned staging buffers: host threads copy chunk i+1 between the
+// caller's memory and pinned memory while the copy engine moves chunk i
+// (the driver's own pageable path is one thread and a narrow 2D copy engine
+// path is slower still).  Pinned sources/destinations are copied directly.
+void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_t st);
+// Rows [0, rows) of a pitched device matrix (row_bytes of each pitch-byte
+// row) into a packed host array: pitched 1D chunks D2H, un-pitched by host
+// threads (no narrow-row 2D copies).  Synchronous.
+void d2h_unpitch(void* dst_host, const uint8_t* src_dev, uint64_t rows, uint32_t row_bytes, uint32_t pitch,
+                 cudaStream_t st);
+
 // Open from a byte source: parse, allocate, stream rows into pitched HBM.
 // With hbm_budget > 0 and a pitched payload larger than it, open in the
 // host-resident streaming mode with two staging buffers of hbm_budget/2.
