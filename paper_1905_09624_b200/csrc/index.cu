@@ -35,7 +35,7 @@ void PinnedBuf::reserve(size_t n) {
     if (ptr) cudaFreeHost(ptr);
     ptr = nullptr;
     bytes = 0;
-    COBS_CUDA(cudaMallocHost(&ptr, n));
+    COBS_CUDA(cudaHostAlloc(&ptr, n, cudaHostAllocPortable)); // pinned for every device's context
     bytes = n;
 }
 PinnedBuf::~PinnedBuf() {

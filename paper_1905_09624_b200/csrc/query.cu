@@ -616,7 +616,7 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     } else {
         ws.pats.reserve(std::max<uint64_t>(h_off[n], 1));
         ws.offs.reserve(sizeof(uint64_t) * (n + 1));
-        COBS_CUDA(cudaMemcpyAsync(ws.pats.ptr, patterns, h_off[n], cudaMemcpyHostToDevice, st));
+        h2d_staged(ws.pats.ptr, patterns, h_off[n], st); // pinned: one async copy; pageable: staged
         COBS_CUDA(cudaMemcpyAsync(ws.offs.ptr, offsets, sizeof(uint64_t) * (n + 1),
                                   cudaMemcpyHostToDevice, st));
         d_pats = ws.pats.as<uint8_t>();
