@@ -207,7 +207,7 @@ struct PcDoc {
     uint32_t nbk;            // buckets (a power of two)
     uint32_t shift;          // 64 - log2(nbk); 64 = a single bucket
     uint32_t doc;            // global document index
-    uint32_t pad;
+    uint32_t sb0;            // two-level scatter: first super-bucket (wave-relative prefix)
 };
 
 struct PcArgs {
@@ -219,10 +219,18 @@ struct PcArgs {
     uint32_t* cursor;         // per bucket write cursor (= exclusive scan of bucket_cnt)
     unsigned long long* keys; // code + 1, grouped by bucket
     unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
+    uint32_t* chunk_sup;      // two-level: per (chunk, super-bucket) key counts [chunk][kSup], or null
 };
 
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix_code(code) >> shift);
+}
+
+constexpr uint32_t kSupLog2 = 5;             // two-level scatter: <= 32 super-buckets per document (A/B: 64 and 256 slower)
+constexpr uint32_t kSup = 1u << kSupLog2;
+__device__ __forceinline__ uint32_t pc_super_shift(const PcDoc& D) { // bucket >> this = super-bucket
+    const uint32_t lg = 64u - D.shift;                               // log2(nbk)
+    return lg - min(lg, kSupLog2);
 }
 
 // chunk c -> its document (last i with docs[i].chunk0 <= c, skipping empty ones)
@@ -292,6 +300,14 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
         if (local)
             for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x)
                 if (s_hist[j]) atomicAdd(&p.bucket_cnt[D.bucket0 + j], s_hist[j]);
+        if (local && p.chunk_sup) { // the two-level scatter's per-chunk super-bucket counts
+            const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
+            if (threadIdx.x < nsb) {
+                uint32_t sum = 0;
+                for (uint32_t j = threadIdx.x << sbs; j < (threadIdx.x + 1u) << sbs; ++j) sum += s_hist[j];
+                p.chunk_sup[c * kSup + threadIdx.x] = sum;
+            }
+        }
         if (threadIdx.x == 0 && s_bad) atomicAdd(p.bad, s_bad);
     }
 }
@@ -345,6 +361,133 @@ __global__ void __launch_bounds__(256) pc_scatter_kernel(PcArgs p) {
             const uint32_t b = pc_bucket(code, D.shift);
             p.keys[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = code + 1ull;
         });
+    }
+}
+
+// ---- two-level scatter: keys first into <= kSup super-buckets per document
+// (a super-bucket = consecutive buckets, so its region is theirs in the
+// final layout), long runs per chunk; then one CTA per super-bucket places
+// its keys into their buckets.  A chunk's runs are then ~512 keys instead of
+// ~16, so DRAM sees whole sectors instead of read-modify-writes of sectors
+// shared with runs written by other CTAs much later.
+
+// super-bucket cursors = offset of its first bucket; super -> document map
+__global__ void pc_super_init_kernel(const PcDoc* docs, uint32_t ndocs, const uint32_t* off, uint32_t* sup_cursor,
+                                     uint32_t* sup_doc) {
+    for (uint32_t i = blockIdx.x; i < ndocs; i += gridDim.x) {
+        const PcDoc D = docs[i];
+        const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
+        for (uint32_t j = threadIdx.x; j < nsb; j += blockDim.x) {
+            sup_cursor[D.sb0 + j] = off[D.bucket0 + (static_cast<uint64_t>(j) << sbs)];
+            sup_doc[D.sb0 + j] = i;
+        }
+    }
+}
+
+template <int QC>
+__global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_t* sup_cursor) {
+    __shared__ uint32_t s_cnt[kSup], s_base[kSup];
+    __shared__ uint32_t s_doc;
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
+        __syncthreads();
+        const PcDoc D = p.docs[s_doc];
+        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
+        const bool counted = p.chunk_sup && D.nbk <= kPcHist; // the histogram pass left the counts
+        if (threadIdx.x < kSup) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
+        if (!counted)
+            pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+                if (dna) atomicAdd(&s_cnt[pc_bucket(code, D.shift) >> sbs], 1u);
+            });
+        __syncthreads();
+        if (threadIdx.x < nsb) {
+            const uint32_t n = counted ? p.chunk_sup[c * kSup + threadIdx.x] : s_cnt[threadIdx.x];
+            if (n) s_base[threadIdx.x] = atomicAdd(&sup_cursor[D.sb0 + threadIdx.x], n);
+            s_cnt[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            if (!dna) return;
+            const uint32_t sb = pc_bucket(code, D.shift) >> sbs;
+            p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = code + 1ull;
+        });
+    }
+}
+
+// one CTA per super-bucket: its keys (in keys_a) into their buckets (keys_b),
+// a tile of kFinTile keys at a time: counting-sorted by bucket in shared
+// memory, then each bucket's run of the tile written with coalesced stores
+// (whole sectors, no read-modify-write of partially written ones).
+constexpr uint32_t kFinTile = 4096;
+constexpr uint32_t kFinPer = kFinTile / 256; // keys per thread per tile
+__global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs, const uint32_t* sup_doc,
+                                                               uint64_t nsup, const uint32_t* off,
+                                                               const unsigned long long* keys_a,
+                                                               unsigned long long* keys_b) {
+    constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
+    __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB];
+    __shared__ unsigned long long s_sorted[kFinTile];
+    __shared__ uint8_t s_lb[kFinTile];
+    for (uint64_t g = blockIdx.x; g < nsup; g += gridDim.x) {
+        const PcDoc D = docs[sup_doc[g]];
+        const uint32_t sbs = pc_super_shift(D), bps = 1u << sbs;
+        const uint64_t b_lo = D.bucket0 + ((g - D.sb0) << sbs);
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] = off[b_lo + t];
+        const uint32_t k0 = off[b_lo], k1 = off[b_lo + bps];
+        for (uint32_t tile = k0; tile < k1; tile += kFinTile) {
+            const uint32_t n = min(kFinTile, k1 - tile);
+            for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cnt[t] = 0;
+            __syncthreads();
+            unsigned long long kv[kFinPer];
+            uint32_t lr[kFinPer]; // bucket (low 8 bits) | rank within the tile's bucket << 8
+#pragma unroll
+            for (uint32_t u = 0; u < kFinPer; ++u) {
+                const uint32_t i = threadIdx.x + u * blockDim.x;
+                kv[u] = i < n ? __ldcs(keys_a + tile + i) : 0ull;
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kFinPer; ++u) {
+                lr[u] = 0;
+                if (kv[u]) {
+                    const uint32_t lb = pc_bucket(kv[u] - 1ull, D.shift) & (bps - 1u);
+                    lr[u] = lb | (atomicAdd(&s_cnt[lb], 1u) << 8);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) { // exclusive scan of the tile's bucket counts (<= kMaxB)
+                uint32_t carry = 0;
+                for (uint32_t c0 = 0; c0 < bps; c0 += 32) {
+                    const uint32_t v = c0 + threadIdx.x < bps ? s_cnt[c0 + threadIdx.x] : 0u;
+                    uint32_t incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (threadIdx.x >= static_cast<uint32_t>(o)) incl += y;
+                    }
+                    if (c0 + threadIdx.x < bps) s_start[c0 + threadIdx.x] = carry + incl - v;
+                    carry += __shfl_sync(0xffffffffu, incl, 31);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (uint32_t u = 0; u < kFinPer; ++u)
+                if (kv[u]) {
+                    const uint32_t pos = s_start[lr[u] & 0xffu] + (lr[u] >> 8);
+                    s_sorted[pos] = kv[u];
+                    s_lb[pos] = static_cast<uint8_t>(lr[u] & 0xffu);
+                }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) { // consecutive i -> consecutive addresses per run
+                const uint32_t lb = s_lb[i];
+                keys_b[s_cur[lb] + (i - s_start[lb])] = s_sorted[i];
+            }
+            __syncthreads();
+            for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] += s_cnt[t];
+        }
     }
 }
 
@@ -742,18 +885,20 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         // bucket too skewed for its set is recounted by hashset_count
         auto partitioned_count = [&] {
             COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            uint64_t kmax = std::min<uint64_t>((free_b / 2) / 8, 0xffffffffull);
+            const char* two_env = std::getenv("COBS_PC_TWO_LEVEL");
+            const bool two_level = two_env ? two_env[0] != '0' : true;
+            uint64_t kmax = std::min<uint64_t>((free_b / 2) / (two_level ? 16 : 8), 0xffffffffull);
             if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
             const uint64_t max_buckets = kmax / (kPcTarget / 2) + 2 * n_docs + 1;
             // plan every wave up front (documents in order, keys <= kmax); the
             // waves then run back to back without a host round trip
-            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys; };
+            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup; };
             std::vector<PcWave> pw;
             std::vector<PcDoc> pd;
             std::vector<std::pair<uint64_t, uint64_t>> oversize; // documents beyond the key buffer
             for (uint64_t d0 = 0; d0 < n_docs;) {
-                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0};
+                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0, 0};
                 uint64_t d1 = d0;
                 while (d1 < n_docs) {
                     const uint64_t W = doc_w[d1];
@@ -775,7 +920,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     D.nbk = static_cast<uint32_t>(nbk);
                     D.shift = 64 - static_cast<uint32_t>(__builtin_ctzll(nbk));
                     D.doc = static_cast<uint32_t>(d1);
+                    D.sb0 = static_cast<uint32_t>(wv.nsup);
                     pd.push_back(D);
+                    wv.nsup += std::min<uint64_t>(nbk, kSup);
                     wv.keys += W;
                     wv.nbuck += nbk;
                     wv.nchunk += (D.run_hi - D.run_lo + kPcRuns - 1) / kPcRuns;
@@ -790,13 +937,23 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 }
                 d0 = d1;
             }
-            uint64_t max_keys = 1, max_nbuck = 1;
+            uint64_t max_keys = 1, max_nbuck = 1, max_nsup = 1;
             for (const PcWave& wv : pw) {
                 max_keys = std::max(max_keys, wv.keys);
                 max_nbuck = std::max(max_nbuck, wv.nbuck);
+                max_nsup = std::max(max_nsup, wv.nsup);
             }
-            DevBuf d_keys, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc;
+            DevBuf d_keys, d_keys_a, d_sup_cur, d_sup_doc, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc;
             d_keys.reserve(8 * max_keys);
+            uint64_t max_nchunk = 1;
+            for (const PcWave& wv : pw) max_nchunk = std::max(max_nchunk, wv.nchunk);
+            DevBuf d_chunk_sup;
+            if (two_level) {
+                d_chunk_sup.reserve(4ull * kSup * max_nchunk);
+                d_keys_a.reserve(8 * max_keys);
+                d_sup_cur.reserve(4 * max_nsup);
+                d_sup_doc.reserve(4 * max_nsup);
+            }
             d_flags.reserve(16 * std::max<size_t>(pw.size(), 1));
             d_cnt.reserve(4 * (max_nbuck + 1));
             d_off.reserve(4 * (max_nbuck + 1));
@@ -828,6 +985,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pa.bucket_cnt = d_cnt.as<uint32_t>();
                 pa.keys = d_keys.as<unsigned long long>();
                 pa.bad = flags;
+                pa.chunk_sup = two_level ? d_chunk_sup.as<uint32_t>() : nullptr;
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
                 if (wv.nchunk) hist<<<grid, 256, 0, st>>>(pa);
                 size_t tb = d_tmp.bytes;
@@ -836,8 +994,20 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 // the scan is both the dedup's bucket offsets and (a copy) the scatter cursors
                 COBS_CUDA(cudaMemcpyAsync(d_cnt.ptr, d_off.ptr, 4 * (wv.nbuck + 1), cudaMemcpyDeviceToDevice, st));
                 pa.cursor = d_cnt.as<uint32_t>();
+                if (wv.nchunk && two_level) {
+                    pc_super_init_kernel<<<std::min<uint32_t>(nd, 148 * 8), kSup, 0, st>>>(
+                        d_docs.as<PcDoc>() + wv.doc0, nd, d_off.as<uint32_t>(), d_sup_cur.as<uint32_t>(),
+                        d_sup_doc.as<uint32_t>());
+                    PcArgs pb = pa;
+                    pb.keys = d_keys_a.as<unsigned long long>();
+                    (q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>)<<<grid, 256, 0, st>>>(
+                        pb, d_sup_cur.as<uint32_t>());
+                    pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
+                        d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
+                        d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
+                }
                 if (wv.nchunk) {
-                    scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
+                    if (!two_level) scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
                     pc_dedup_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), 256, wv.slots * 8, st>>>(
                         d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
                         d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
@@ -851,6 +1021,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 16 * pw.size(), cudaMemcpyDeviceToHost, st));
             COBS_CUDA(cudaStreamSynchronize(st));
             d_keys.release(); // before any recount needs the memory
+            d_keys_a.release();
             bool byte_windows = !oversize.empty();
             for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
             if (!byte_windows) fill_rpt = kFillRunsDna;
