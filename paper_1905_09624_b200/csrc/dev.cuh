@@ -232,8 +232,8 @@ namespace cobsg {
 //     the canonical min(gram, revcomp) (termizer.cpp:117-118) a 64-bit min;
 //   * the code is an exact (injective) dedup key -- no byte compares;
 //   * forward and reverse-complement codes roll in O(1) per window;
-//   * the ASCII bytes XXH64 needs are rebuilt from the code in registers with
-//     one PRMT per 4 bases.
+//   * the ASCII bytes XXH64 needs are rebuilt from the code in registers
+//     (bases spread to nibbles, one PRMT per 4 bases).
 // Windows with any other byte take the byte path above.
 
 // 1 iff c is one of 'A','C','G','T': all four lie in 0x40..0x5f at bit
@@ -244,23 +244,32 @@ __device__ __forceinline__ uint32_t acgt_bit(uint32_t c) {
 // 2-bit code of an A/C/G/T byte: ((c >> 1) ^ (c >> 2)) & 3 maps A,C,G,T to 0..3.
 __device__ __forceinline__ uint32_t base_code(uint32_t c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
 
-// ASCII of 4 bases given as 8 code bits (first base in bits 7..6), as a
-// little-endian word: PRMT with nibble selectors = the 2-bit codes.
-__device__ __forceinline__ uint32_t bases4_ascii(uint32_t b8) {
-    uint32_t sel = (b8 >> 6) | (b8 & 0x30u) | ((b8 & 0x0cu) << 6) | ((b8 & 0x03u) << 12);
-    return __byte_perm(0x54474341u, 0u, sel);
+// The term's bases in little-endian order: base j of a q-base code in bits
+// 2j, 2j+1 (the code has base 0 most significant).
+__device__ __forceinline__ uint64_t code_le(uint64_t code, uint32_t q) {
+    uint64_t x = __brevll(code); // reverses the bases and the 2 bits within each
+    x = ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+    return x >> (64 - 2 * q);
 }
-
-// ASCII word of bases [i, i+4) of a q-base code (i + 4 <= q).
-__device__ __forceinline__ uint32_t code_word(uint64_t code, uint32_t q, uint32_t i) {
-    return bases4_ascii(static_cast<uint32_t>(code >> (2 * (q - 4 - i))) & 0xffu);
+// ASCII of bases [i, i+8) / [i, i+4) / i of a little-endian code: each base's
+// 2 bits are spread to a nibble (shift-or-mask steps), and PRMT selects
+// "ACGT"[nibble] for 4 bytes at a time.
+__device__ __forceinline__ uint64_t le_lane64(uint64_t le, uint32_t i) {
+    uint32_t x = static_cast<uint32_t>(le >> (2 * i)) & 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u; // nibble k = base i + k
+    return static_cast<uint64_t>(__byte_perm(0x54474341u, 0u, x)) |
+           (static_cast<uint64_t>(__byte_perm(0x54474341u, 0u, x >> 16)) << 32);
 }
-__device__ __forceinline__ uint32_t code_byte(uint64_t code, uint32_t q, uint32_t i) {
-    return __byte_perm(0x54474341u, 0u, static_cast<uint32_t>(code >> (2 * (q - 1 - i))) & 3u) & 0xffu;
+__device__ __forceinline__ uint32_t le_word(uint64_t le, uint32_t i) {
+    uint32_t x = static_cast<uint32_t>(le >> (2 * i)) & 0xffu;
+    x = (x | (x << 4)) & 0x0f0fu;
+    x = (x | (x << 2)) & 0x3333u;
+    return __byte_perm(0x54474341u, 0u, x);
 }
-__device__ __forceinline__ uint64_t code_lane64(uint64_t code, uint32_t q, uint32_t i) {
-    return static_cast<uint64_t>(code_word(code, q, i)) |
-           (static_cast<uint64_t>(code_word(code, q, i + 4)) << 32);
+__device__ __forceinline__ uint32_t le_byte(uint64_t le, uint32_t i) {
+    return __byte_perm(0x54474341u, 0u, static_cast<uint32_t>(le >> (2 * i)) & 3u) & 0xffu;
 }
 
 // XXH64 of the ASCII bytes of a q-base code, 1 <= q <= 32 (QC = q when known
@@ -269,13 +278,14 @@ template <int QC>
 __device__ __forceinline__ uint64_t xxh64_code(uint64_t code, uint32_t q_rt, uint64_t seed) {
     using namespace xx;
     const uint32_t q = QC ? QC : q_rt;
+    const uint64_t le = code_le(code, q);
     uint32_t i = 0;
     uint64_t h;
     if (q == 32) { // one 32-byte stripe
-        uint64_t v1 = rnd(seed + P1 + P2, code_lane64(code, q, 0));
-        uint64_t v2 = rnd(seed + P2, code_lane64(code, q, 8));
-        uint64_t v3 = rnd(seed, code_lane64(code, q, 16));
-        uint64_t v4 = rnd(seed - P1, code_lane64(code, q, 24));
+        uint64_t v1 = rnd(seed + P1 + P2, le_lane64(le, 0));
+        uint64_t v2 = rnd(seed + P2, le_lane64(le, 8));
+        uint64_t v3 = rnd(seed, le_lane64(le, 16));
+        uint64_t v4 = rnd(seed - P1, le_lane64(le, 24));
         h = rotl(v1, 1) + rotl(v2, 7) + rotl(v3, 12) + rotl(v4, 18);
         h = (h ^ rnd(0, v1)) * P1 + P4;
         h = (h ^ rnd(0, v2)) * P1 + P4;
@@ -289,17 +299,17 @@ __device__ __forceinline__ uint64_t xxh64_code(uint64_t code, uint32_t q_rt, uin
 #pragma unroll
     for (int l = 0; l < 4; ++l)
         if (i + 8 <= q) {
-            h = rotl(h ^ rnd(0, code_lane64(code, q, i)), 27) * P1 + P4;
+            h = rotl(h ^ rnd(0, le_lane64(le, i)), 27) * P1 + P4;
             i += 8;
         }
     if (i + 4 <= q) {
-        h = rotl(h ^ ((uint64_t)code_word(code, q, i) * P1), 23) * P2 + P3;
+        h = rotl(h ^ (static_cast<uint64_t>(le_word(le, i)) * P1), 23) * P2 + P3;
         i += 4;
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b)
         if (i < q) {
-            h = rotl(h ^ ((uint64_t)code_byte(code, q, i) * P5), 11) * P1;
+            h = rotl(h ^ (static_cast<uint64_t>(le_byte(le, i)) * P5), 11) * P1;
             ++i;
         }
     h ^= h >> 33;
