@@ -27,6 +27,7 @@
 #include <cstring>
 #include <fstream>
 #include <numeric>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 
@@ -98,12 +99,16 @@ __device__ __forceinline__ void roll_windows(const uint8_t* sb, uint64_t j0, uin
 // [j0, j1 + q - 1) are pushed in order (aligned uint4 loads for the body,
 // bytes at the ragged ends), f(j, dna, code) after every complete window j
 // in [j0, j1).  Only for q <= 32.
-template <int QC, int UNROLL = 4, typename F>
+template <int QC, int UNROLL = 4, int SB = 0, typename F>
 __device__ __forceinline__ void roll_range(const uint8_t* sb, uint64_t j0, uint64_t j1, uint32_t q_rt,
-                                           bool canonical, F&& f) {
+                                           bool canonical, F&& f, const uint8_t* symtab = nullptr) {
     const uint32_t q = QC ? QC : q_rt;
     if (j1 <= j0) return;
-    Roller R(q);
+    // SB > 0: small-alphabet symbol codes (non-canonical raw bytes), else 2-bit DNA codes
+    typename std::conditional<SB == 0, Roller, SymRoller<SB ? SB : 1>>::type R = [&] {
+        if constexpr (SB == 0) return Roller(q);
+        else return SymRoller<SB>(q, symtab);
+    }();
     const uint64_t end = j1 + q - 1, first = j0 + q - 1;
     uint64_t i = j0;
     auto push = [&](uint32_t c) {
@@ -220,12 +225,14 @@ struct PcArgs {
     unsigned long long* keys; // code + 1, grouped by bucket
     unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
     uint32_t* chunk_sup;      // two-level: per (chunk, super-bucket) key counts [chunk][kSup], or null
+    const uint8_t* symtab;    // SB > 0: byte -> symbol index (256 entries)
 };
 
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix_code(code) >> shift);
 }
 
+constexpr int kSymBits = 5;                  // symbol codes: <= 32 distinct byte values, q <= 12
 constexpr uint32_t kSupLog2 = 5;             // two-level scatter: <= 32 super-buckets per document (A/B: 64 and 256 slower)
 constexpr uint32_t kSup = 1u << kSupLog2;
 __device__ __forceinline__ uint32_t pc_super_shift(const PcDoc& D) { // bucket >> this = super-bucket
@@ -248,8 +255,9 @@ __device__ __forceinline__ uint32_t pc_chunk_doc(const PcDoc* docs, uint32_t n, 
 
 // f(dna, code) for every window of the chunk's runs; each thread rolls
 // through kPcRunsPerThread consecutive runs (256 threads per CTA)
-template <int QC, typename F>
-__device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uint64_t r0, uint64_t r1, F&& f) {
+template <int QC, int SB = 0, typename F>
+__device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uint64_t r0, uint64_t r1, F&& f,
+                                           const uint8_t* symtab = nullptr) {
     const uint32_t q = QC ? QC : a.q;
     uint64_t g = r0 + static_cast<uint64_t>(threadIdx.x) * kPcRunsPerThread;
     const uint64_t ge = min(r1, g + kPcRunsPerThread);
@@ -259,17 +267,19 @@ __device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uin
         const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
         const uint64_t W = len >= q ? len - q + 1 : 0;
         const uint64_t gend = min(ge, a.seg_rbase[s + 1]);
-        roll_range<QC>(a.seqs + a.seg_off[s], (g - rb) * kBRun, min(W, (gend - rb) * kBRun), q, a.canonical != 0,
-                       [&](uint64_t, bool dna, uint64_t code) { f(dna, code); });
+        roll_range<QC, 4, SB>(a.seqs + a.seg_off[s], (g - rb) * kBRun, min(W, (gend - rb) * kBRun), q,
+                              a.canonical != 0, [&](uint64_t, bool dna, uint64_t code) { f(dna, code); }, symtab);
         g = gend;
     }
 }
 
-template <int QC>
+template <int QC, int SB = 0>
 __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
     __shared__ uint32_t s_hist[kPcHist];
     __shared__ uint32_t s_doc;
     __shared__ unsigned long long s_bad;
+    __shared__ uint8_t s_sym[256];
+    if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
         __syncthreads();
         const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
         uint32_t bad = 0;
-        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+        pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
             if (!dna) { // canonical: skipped (termizer.cpp:113-116); else needs the byte path
                 bad += p.a.canonical ? 0u : 1u;
                 return;
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
                 atomicAdd(&s_hist[b], 1u);
             else
                 atomicAdd(&p.bucket_cnt[D.bucket0 + b], 1u);
-        });
+        }, s_sym);
         if (bad) atomicAdd(&s_bad, (unsigned long long)bad);
         __syncthreads();
         if (local)
@@ -384,10 +394,12 @@ __global__ void pc_super_init_kernel(const PcDoc* docs, uint32_t ndocs, const ui
     }
 }
 
-template <int QC>
+template <int QC, int SB = 0>
 __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_t* sup_cursor) {
     __shared__ uint32_t s_cnt[kSup], s_base[kSup];
     __shared__ uint32_t s_doc;
+    __shared__ uint8_t s_sym[256];
+    if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         __syncthreads();
         if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
@@ -399,9 +411,9 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
         if (threadIdx.x < kSup) s_cnt[threadIdx.x] = 0;
         __syncthreads();
         if (!counted)
-            pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
                 if (dna) atomicAdd(&s_cnt[pc_bucket(code, D.shift) >> sbs], 1u);
-            });
+            }, s_sym);
         __syncthreads();
         if (threadIdx.x < nsb) {
             const uint32_t n = counted ? p.chunk_sup[c * kSup + threadIdx.x] : s_cnt[threadIdx.x];
@@ -409,11 +421,11 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
             s_cnt[threadIdx.x] = 0;
         }
         __syncthreads();
-        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+        pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
             if (!dna) return;
             const uint32_t sb = pc_bucket(code, D.shift) >> sbs;
             p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = code + 1ull;
-        });
+        }, s_sym);
     }
 }
 
@@ -510,6 +522,34 @@ __global__ void any_non_acgt_kernel(const uint8_t* p, uint64_t n, unsigned int* 
     for (uint64_t i = head + nv * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
         bad |= !acgt_bit(p[i]);
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(found, 1u);
+}
+
+// the set of byte values in [0, n) as a 256-bit mask (8 words)
+__global__ void byte_set_kernel(const uint8_t* p, uint64_t n, unsigned int* set) {
+    uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto add = [&](uint32_t b) {
+        const uint32_t bit = 1u << (b & 31u), w = b >> 5;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[k] |= w == static_cast<uint32_t>(k) ? bit : 0u;
+    };
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t align = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+    const uint64_t head = n < align ? n : align;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < head; i += stride) add(p[i]);
+    const uint4* v = reinterpret_cast<const uint4*>(p + head);
+    const uint64_t nv = (n - head) / 16;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 x = __ldcs(v + i);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) add((w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    }
+    for (uint64_t i = head + nv * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) add(p[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t r = __reduce_or_sync(0xffffffffu, m[k]);
+        if ((threadIdx.x & 31) == 0 && r) atomicOr(set + k, r);
+    }
 }
 
 // bucket -> document of a wave
@@ -879,6 +919,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             COBS_CUDA(cudaStreamSynchronize(st)); // tables die with this scope
         };
 
+        // symbol codes for raw-byte corpora over a small alphabet (see SymRoller)
+        uint32_t sym_bits = 0;
+        DevBuf d_symtab;
+        d_symtab.reserve(256);
+
         // partitioned count for q <= 32 (see pc_hist_kernel), in waves of
         // documents whose windows fit the key buffer; a wave that meets a
         // window needing the byte path (non-ACGT, no canonicalisation) or a
@@ -886,7 +931,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         auto partitioned_count = [&] {
             COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
             const char* two_env = std::getenv("COBS_PC_TWO_LEVEL");
-            const bool two_level = two_env ? two_env[0] != '0' : true;
+            const bool two_level = sym_bits || (two_env ? two_env[0] != '0' : true); // symbol codes: two-level only
             uint64_t kmax = std::min<uint64_t>((free_b / 2) / (two_level ? 16 : 8), 0xffffffffull);
             if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
@@ -966,7 +1011,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             if (!pd.empty())
                 COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
             COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
-            auto hist = q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
+            auto hist = sym_bits ? pc_hist_kernel<0, kSymBits> : q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
             auto scat = q == 31 ? pc_scatter_kernel<31> : pc_scatter_kernel<0>;
             COBS_CUDA(cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
             COBS_CUDA(cudaFuncSetAttribute(pc_dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
@@ -986,6 +1031,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pa.keys = d_keys.as<unsigned long long>();
                 pa.bad = flags;
                 pa.chunk_sup = two_level ? d_chunk_sup.as<uint32_t>() : nullptr;
+                pa.symtab = d_symtab.as<uint8_t>();
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
                 if (wv.nchunk) hist<<<grid, 256, 0, st>>>(pa);
                 size_t tb = d_tmp.bytes;
@@ -1000,7 +1046,8 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                         d_sup_doc.as<uint32_t>());
                     PcArgs pb = pa;
                     pb.keys = d_keys_a.as<unsigned long long>();
-                    (q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>)<<<grid, 256, 0, st>>>(
+                    (sym_bits ? pc_scatter_super_kernel<0, kSymBits>
+                              : q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>)<<<grid, 256, 0, st>>>(
                         pb, d_sup_cur.as<uint32_t>());
                     pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
                         d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
@@ -1022,7 +1069,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             COBS_CUDA(cudaStreamSynchronize(st));
             d_keys.release(); // before any recount needs the memory
             d_keys_a.release();
-            bool byte_windows = !oversize.empty();
+            bool byte_windows = !oversize.empty() || sym_bits; // symbol-coded windows hash their bytes in the fill
             for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
             if (!byte_windows) fill_rpt = kFillRunsDna;
             for (size_t i = 0; i < pw.size(); ++i)
@@ -1052,6 +1099,27 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             COBS_CUDA(cudaMemcpyAsync(&found, d_found.ptr, 4, cudaMemcpyDeviceToHost, st));
             COBS_CUDA(cudaStreamSynchronize(st));
             use_pc = found == 0;
+            const char* sym_env = std::getenv("COBS_PC_SYMBOLS");
+            if (found && q * kSymBits <= 62 && !(sym_env && sym_env[0] == '0')) {
+                // raw bytes: if the corpus has <= 2^kSymBits distinct byte values, every
+                // window is an exact kSymBits-per-symbol code and the partitioned count applies
+                DevBuf d_set;
+                d_set.reserve(32);
+                COBS_CUDA(cudaMemsetAsync(d_set.ptr, 0, 32, st));
+                byte_set_kernel<<<148 * 8, 256, 0, st>>>(wa.seqs, total_bytes, d_set.as<unsigned int>());
+                uint32_t set[8];
+                COBS_CUDA(cudaMemcpyAsync(set, d_set.ptr, 32, cudaMemcpyDeviceToHost, st));
+                COBS_CUDA(cudaStreamSynchronize(st));
+                std::vector<uint8_t> tab(256, 0xff);
+                uint32_t nsym = 0;
+                for (uint32_t b = 0; b < 256; ++b)
+                    if ((set[b >> 5] >> (b & 31)) & 1u) tab[b] = static_cast<uint8_t>(nsym++);
+                if (nsym <= (1u << kSymBits)) {
+                    COBS_CUDA(cudaMemcpyAsync(d_symtab.ptr, tab.data(), 256, cudaMemcpyHostToDevice, st));
+                    sym_bits = kSymBits;
+                    use_pc = true;
+                }
+            }
         }
         if (use_pc)
             partitioned_count();

@@ -339,6 +339,27 @@ struct Roller {
     __device__ __forceinline__ uint64_t canon() const { return fwd < rev ? fwd : rev; }
 };
 
+// Rolling codes of windows over a small alphabet (<= 2^SB byte values, q*SB
+// <= 62 bits): a window's code is its q symbols' SB-bit indices (table
+// `tab`: byte -> index, 0xff = not in the alphabet), first symbol most
+// significant.  An exact (injective) key for raw-byte windows, used only to
+// count distinct windows; the row hashes still come from the bytes.
+template <int SB>
+struct SymRoller {
+    uint64_t fwd = 0, mask;
+    uint32_t q, since_bad = 0;
+    const uint8_t* tab;
+    __device__ SymRoller(uint32_t q_, const uint8_t* t)
+        : mask(q_ * SB >= 64 ? ~0ull : ((1ull << (q_ * SB)) - 1)), q(q_), tab(t) {}
+    __device__ __forceinline__ void push(uint32_t c) {
+        const uint32_t sym = tab[c];
+        fwd = ((fwd << SB) | (sym & ((1u << SB) - 1u))) & mask;
+        since_bad = sym != 0xffu ? since_bad + 1 : 0;
+    }
+    __device__ __forceinline__ bool dna() const { return since_bad >= q; } // (a complete window)
+    __device__ __forceinline__ uint64_t canon() const { return fwd; }
+};
+
 // Slot hash for code-keyed sets where the XXH64 row hash is not needed
 // (the splitmix64 finaliser: two multiplies).
 __device__ __forceinline__ uint64_t mix_code(uint64_t z) {

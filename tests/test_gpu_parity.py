@@ -471,6 +471,28 @@ def test_count_partitioned_vs_hashset(gpu):
                               COBS_PC_WAVE_KEYS=150000) == want
 
 
+def test_count_partitioned_symbol_codes(gpu):
+    """Raw-byte corpora over a small alphabet (<= 32 byte values, q <= 12)
+    take the partitioned count with 5-bit symbol codes (SymRoller): the same
+    file as the oracle and as the hash-set count, for a protein corpus (the
+    config-4 shape), DNA with N at q = 12, several waves; a corpus with more
+    than 32 byte values stays on the hash sets."""
+    rng = random.Random(77)
+    prot = b"ACDEFGHIKLMNPQRSTVWY"
+    cases = [
+        (10, [(b"p%03d" % i, [rand(rng, rng.choice([0, 5, 10, 300, 4000]), prot)]) for i in range(50)]
+         + [(b"rep", [b"MKV" * 3000]), (b"multi", [rand(rng, 500, prot), b"", rand(rng, 9, prot)])]),
+        (12, [(b"n%03d" % i, [rand(rng, rng.choice([12, 800, 3000]), b"ACGTN")]) for i in range(40)]),
+        (8, [(b"w%03d" % i, [bytes(rng.randrange(40, 120) for _ in range(600))]) for i in range(20)]),
+    ]
+    for q, docs in cases:
+        params = cb.IndexParams(q=q, k=2, p=0.2, block_size=16)
+        want = O.build_image(docs, q=q, k=2, p=0.2, block_size=16, kind=1)
+        assert _build_env(docs, params, cb.KIND_COMPACT) == want, q
+        assert _build_env(docs, params, cb.KIND_COMPACT, COBS_PC_SYMBOLS=0) == want, q
+        assert _build_env(docs, params, cb.KIND_COMPACT, COBS_PC_WAVE_KEYS=3000) == want, q
+
+
 def test_count_partitioned_huge_document(gpu):
     """A document with more buckets than a chunk histogram holds in shared
     memory (> 8,192 x 4,096 windows): global-cursor scatter path."""
