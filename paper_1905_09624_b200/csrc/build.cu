@@ -689,16 +689,28 @@ __global__ void __launch_bounds__(256) slab_fill_kernel(WinArgs a, const SlabDoc
             auto put = [&](uint64_t j, bool dna, uint64_t code) {
                 const uint8_t* w = sb + j;
                 if (dna) {
-                    for (uint32_t seed = 0; seed < a.k; ++seed)
-                        atomicOr(col + fastmod(xxh64_code<QC>(code, q, seed), D.w, D.magic), bit);
+                    if (a.k > 1 && q < 32) { // the seeds share the seed-independent multiplies
+                        const XxhShort x = xxh_short_code<QC>(code, q);
+                        for (uint32_t seed = 0; seed < a.k; ++seed)
+                            atomicOr(col + fastmod(xxh_short_seed<QC>(x, q, seed), D.w, D.magic), bit);
+                    } else {
+                        for (uint32_t seed = 0; seed < a.k; ++seed)
+                            atomicOr(col + fastmod(xxh64_code<QC>(code, q, seed), D.w, D.magic), bit);
+                    }
                 } else if (a.canonical) {
                     if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
                     const bool rc = choose_rc(w, q);
                     for (uint32_t seed = 0; seed < a.k; ++seed)
                         atomicOr(col + fastmod(xxh64_term(w, q, rc, seed), D.w, D.magic), bit);
                 } else {
-                    for (uint32_t seed = 0; seed < a.k; ++seed)
-                        atomicOr(col + fastmod(xxh64_term(w, q, false, seed), D.w, D.magic), bit);
+                    if (a.k > 1 && q < 32) {
+                        const XxhShort x = xxh_short_term(w, q, false);
+                        for (uint32_t seed = 0; seed < a.k; ++seed)
+                            atomicOr(col + fastmod(xxh_short_seed<0>(x, q, seed), D.w, D.magic), bit);
+                    } else {
+                        for (uint32_t seed = 0; seed < a.k; ++seed)
+                            atomicOr(col + fastmod(xxh64_term(w, q, false, seed), D.w, D.magic), bit);
+                    }
                 }
             };
             if (rpt == 1)

@@ -320,6 +320,94 @@ __device__ __forceinline__ uint64_t xxh64_code(uint64_t code, uint32_t q_rt, uin
     return h;
 }
 
+// XXH64 of an input shorter than 32 bytes (xxhash64.hpp:68-93) splits into
+// a seed-independent part -- round(0, lane) of each 8-byte lane, word * P1
+// of the 4-byte tail, byte * P5 of each last byte: 12 of the 19 multiplies
+// at q = 31 -- and the accumulator chain that starts at seed + P5 + len.
+// Several seeds of one term (k > 1) share the first part.
+struct XxhShort {
+    uint64_t k8[3], k4, k1[3];
+};
+template <int QC>
+__device__ __forceinline__ XxhShort xxh_short_code(uint64_t code, uint32_t q_rt) { // 1 <= q < 32
+    using namespace xx;
+    const uint32_t q = QC ? QC : q_rt;
+    const uint64_t le = code_le(code, q);
+    XxhShort x{};
+    uint32_t i = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+        if (i + 8 <= q) {
+            x.k8[l] = rnd(0, le_lane64(le, i));
+            i += 8;
+        }
+    if (i + 4 <= q) {
+        x.k4 = static_cast<uint64_t>(le_word(le, i)) * P1;
+        i += 4;
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+        if (i < q) {
+            x.k1[b] = static_cast<uint64_t>(le_byte(le, i)) * P5;
+            ++i;
+        }
+    return x;
+}
+__device__ __forceinline__ XxhShort xxh_short_term(const uint8_t* w, uint32_t q, bool rc) { // 1 <= q < 32
+    using namespace xx;
+    XxhShort x{};
+    uint32_t i = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+        if (i + 8 <= q) {
+            x.k8[l] = rnd(0, term_lane64(w, q, rc, i));
+            i += 8;
+        }
+    if (i + 4 <= q) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 3; b >= 0; --b) v = (v << 8) | term_byte(w, q, rc, i + static_cast<uint32_t>(b));
+        x.k4 = static_cast<uint64_t>(v) * P1;
+        i += 4;
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+        if (i < q) {
+            x.k1[b] = static_cast<uint64_t>(term_byte(w, q, rc, i)) * P5;
+            ++i;
+        }
+    return x;
+}
+template <int QC>
+__device__ __forceinline__ uint64_t xxh_short_seed(const XxhShort& x, uint32_t q_rt, uint64_t seed) {
+    using namespace xx;
+    const uint32_t q = QC ? QC : q_rt;
+    uint64_t h = seed + P5 + q;
+    uint32_t i = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+        if (i + 8 <= q) {
+            h = rotl(h ^ x.k8[l], 27) * P1 + P4;
+            i += 8;
+        }
+    if (i + 4 <= q) {
+        h = rotl(h ^ x.k4, 23) * P2 + P3;
+        i += 4;
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+        if (i < q) {
+            h = rotl(h ^ x.k1[b], 11) * P1;
+            ++i;
+        }
+    h ^= h >> 33;
+    h *= P2;
+    h ^= h >> 29;
+    h *= P3;
+    h ^= h >> 32;
+    return h;
+}
+
 // Rolling 2-bit codes over a run of windows.  push() consumes one byte;
 // after q pushes without a non-ACGT byte in the last q, fwd/rev hold the
 // window's forward and reverse-complement codes.
