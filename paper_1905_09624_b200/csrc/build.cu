@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
                                                     unsigned long long* term_count) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t q = QC ? QC : a.q;
+    const bool codes = codes_exact(q, a.canonical != 0); // else q = 32 raw: byte path
     __shared__ uint64_t s_seg[2];
     const uint64_t nchunks = (a.r_hi - a.r_lo + kChunkRuns - 1) / kChunkRuns;
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
             roll_windows<QC>(sb, j0, j1, q, a.canonical != 0, [&](uint64_t j, bool dna, uint64_t code) {
                 const uint8_t* w = sb + j;
                 const uint32_t pos = static_cast<uint32_t>(w - dbase);
-                if (dna) { // the slot only needs a well-mixed hash of the exact code
+                if (dna && codes) { // the slot only needs a well-mixed hash of the exact code
                     cnt += set_insert_code(t, mask, mix_code(code), code);
                 } else if (a.canonical) {
                     if (q <= 32 || !window_acgt(w, q)) return; // skipped (termizer.cpp:113-116)
@@ -1099,7 +1100,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         // key buffer; COBS_COUNT_PARTITION=1 forces the partitioned count)
         uint64_t total_w = 0;
         for (uint64_t d = 0; d < n_docs; ++d) total_w += doc_w[d];
-        bool use_pc = q <= 32 && (pc_env ? pc_env[0] == '1' : total_w >= (1ull << 30));
+        // (codes_exact: q = 32 without canonicalisation has no spare key value)
+        bool use_pc = codes_exact(q, wa.canonical != 0) &&
+                      (pc_env ? pc_env[0] == '1' : total_w >= (1ull << 30));
         const char* scan_env = std::getenv("COBS_PC_NO_SCAN"); // tests: reach the per-wave fallback
         if (use_pc && !wa.canonical && total_bytes && !(scan_env && scan_env[0] == '1')) {
             // byte-path windows ahead? then the hash sets straight away

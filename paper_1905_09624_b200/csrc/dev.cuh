@@ -458,9 +458,18 @@ __device__ __forceinline__ uint64_t mix_code(uint64_t z) {
     return z ^ (z >> 33);
 }
 
-// Exact set insert keyed by the 2-bit code (bit 63 clear; +1 keeps 0 empty).
-// Byte-path keys (set_insert above) always have bit 63 set when both kinds
-// share a table (see set_insert_tagged), so the key spaces never collide.
+// 2-bit codes are exact, collision-free set keys (code + 1, 0 = empty) iff
+// q < 32, or q = 32 with canonicalisation (min(fwd, revcomp) is never
+// 2^64-1, and canonical mode skips every byte-path window, so no tagged key
+// shares the table).  Non-canonical q = 32 windows take the byte path.
+__host__ __device__ __forceinline__ bool codes_exact(uint32_t q, bool canonical) {
+    return q < 32 || (q == 32 && canonical);
+}
+
+// Exact set insert keyed by the 2-bit code (+1 keeps 0 empty; see
+// codes_exact for when this is collision-free).  When q < 32 the code has
+// bit 63 clear, and byte-path keys sharing a table (set_insert_tagged)
+// always have bit 63 set, so the key spaces never collide.
 __device__ __forceinline__ bool set_insert_code(unsigned long long* tab, uint64_t mask, uint64_t h,
                                                 uint64_t code) {
     const unsigned long long key = static_cast<unsigned long long>(code) + 1ull;

@@ -131,7 +131,13 @@ __global__ void __launch_bounds__(THREADS) termize_hash_kernel(TermizeArgs a) {
     __shared__ typename Reduce::TempStorage tmp_reduce;
     __shared__ uint32_t s_count; // distinct terms of the current query
     const uint32_t q = QC ? QC : a.q, k = a.k;
-    const bool code_path = q <= 32; // DNA windows carried as 2-bit codes
+    // DNA windows carried as 2-bit codes.  Not for q = 32 without
+    // canonicalisation: there a code spans all 64 bits, so the poly-T code
+    // 2^64-1 would make the key code+1 wrap to the empty marker, and codes
+    // with bit 63 set would share the key space of the byte-path keys --
+    // those patterns take the byte path (exact byte compares) instead.
+    // (Canonical codes at q = 32 are never all ones: revcomp(T^32) = A^32.)
+    const bool code_path = codes_exact(q, a.canonical != 0);
     unsigned long long* s_tab = s_dyn;
     TileView T(reinterpret_cast<uint8_t*>(s_dyn + a.smem_slots));
     for (uint64_t qi = blockIdx.x; qi < a.n; qi += gridDim.x) {

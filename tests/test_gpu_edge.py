@@ -128,3 +128,35 @@ def test_tie_order_with_non_ascii_names(gpu, tmp_path):
         assert [(h.doc_name, h.score) for h in got.hits] == [(all_names[d], s) for d, s in want]
         assert len({h.score for h in got.hits}) == 1  # a genuine tie
     view.close()
+
+
+@pytest.mark.parametrize("partition", ["0", "1"])
+def test_q32_raw_poly_t_and_high_codes(gpu, partition):
+    """q = 32 without canonicalisation: the poly-T 32-mer's 2-bit code is
+    2^64-1 and G/T-leading codes have bit 63 set, so code keys would wrap to
+    the empty marker / share the byte-path key space.  The reference dedups
+    with sort + unique over the term bytes (termizer.cpp:120-127), so T^32
+    is one term however often it occurs.  l, dense scores, hits and the
+    built file bytes must equal the oracle on both count paths
+    (COBS_COUNT_PARTITION=0/1, read per call)."""
+    import os
+    rng = random.Random(3232)
+    T32 = b"T" * 32
+    special = [b"T" * 40, T32 + b"N" + T32, b"G" * 33 + b"T" * 33, T32 + b"A" + T32 + b"N" + b"T" * 35,
+               b"N".join(rb(rng, 40, b"GT") for _ in range(6))]
+    docs = [(b"s%02d" % i, [s]) for i, s in enumerate(special)]
+    docs += [(b"r%02d" % i, [rb(rng, rng.randint(32, 400), b"ACGTN" if i % 2 else b"GT"),
+                              T32 * (i % 3)]) for i in range(20)]
+    pats = special + [T32, T32 + T32, b"T" * 31, T32 + b"N" + T32 + b"G" * 40,
+                      docs[7][1][0] + T32, rb(rng, 200, b"GTN")]
+    os.environ["COBS_COUNT_PARTITION"] = partition
+    try:
+        for kind, block in ((0, 1024), (1, 6)):
+            img = O.build_image(docs, q=32, k=2, canonical=False, block_size=block, kind=kind)
+            params = cb.IndexParams(q=32, k=2, canonical=False, block_size=block)
+            assert cb.build_image(docs, params, kind, device=0) == img
+            idx = O.OracleIndex.parse(img)
+            assert idx.term_counts()[idx.names().index(b"s00")] == 1  # T^40: nine windows, one term
+            check(img, pats, Ks=(1e-12, 0.5, 1.0), tops=(0, 3))
+    finally:
+        del os.environ["COBS_COUNT_PARTITION"]

@@ -144,3 +144,20 @@ def test_c5_header_and_rows_vs_ref():
         a = orc.query(pat, 0.25, scores=True)
         b = parsed.query(pat, 0.25, scores=True)
         assert a[:3] == b[:3] and np.array_equal(a[3], b[3])
+
+
+def test_q32_poly_t_vs_ref():
+    """q = 32, raw bytes: T^32 repeated is one term (sort + unique over the
+    term strings, termizer.cpp:120-127); the oracle's term counts and built
+    file equal the reference's (the GPU edge test checks against these)."""
+    T32 = b"T" * 32
+    content = [b"T" * 40, T32 + b"N" + T32, b"G" * 33 + b"T" * 33]
+    for c in content:
+        assert O.extract_terms([c], 32, False) == O.ref_extract_terms([c], 32, False)
+    assert len(O.extract_terms([b"T" * 40], 32, False)[0]) == 1
+    docs = [(b"s%02d" % i, [c]) for i, c in enumerate(content)]
+    img = O.build_image(docs, q=32, k=2, canonical=False, block_size=2, kind=1)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "q32.cobs")
+        O.ref_build_write(docs, path, q=32, k=2, canonical=False, block_size=2, kind=1)
+        assert open(path, "rb").read() == img
