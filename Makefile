@@ -12,11 +12,12 @@ HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh $(SRC)/*.h) include/cobs_gpu.h
 
 .PHONY: all lib oracle cpptest clean
 all: lib oracle
-lib: $(OUT)/libcobs_gpu.so $(OUT)/libcobs_synth.so
+lib: $(OUT)/libcobs_gpu.so workloads/_lib/libcobs_synth.so
 
-$(OUT)/libcobs_synth.so: $(SRC)/synth_host.c $(SRC)/synth.h
-	@mkdir -p $(OUT)
-	gcc -std=gnu11 -O2 -fPIC -shared -pthread -o $@ $(SRC)/synth_host.c -lm
+# seeded input generator (bench / tests / tools; not the product)
+workloads/_lib/libcobs_synth.so: workloads/synth_host.c $(SRC)/synth.h
+	@mkdir -p workloads/_lib
+	gcc -std=gnu11 -O2 -fPIC -shared -pthread -o $@ workloads/synth_host.c -lm
 
 $(OUT)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OUT)
@@ -54,4 +55,4 @@ oracle/_build/libcobs_oracle.so:
 	$(MAKE) -C oracle oracle
 
 clean:
-	rm -rf $(OUT) oracle/_build
+	rm -rf $(OUT) oracle/_build workloads/_lib

@@ -52,7 +52,40 @@ def parse():
     ap.add_argument("--no-build", action="store_true")
     ap.add_argument("--c5-median", type=float, default=0.0)
     ap.add_argument("--c5-docs", type=int, default=0)
+    ap.add_argument("--c5-block-size", type=int, default=0)
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "blocks"],
+                    help="replicas: every rank holds the whole index and answers its own batch "
+                         "(weak scaling); blocks: every rank holds a block range of the C5 index "
+                         "and answers the whole batch, hit lists merged on rank 0 (strong scaling)")
+    ap.add_argument("--engine", default="cuda", choices=["cuda", "oracle"],
+                    help=argparse.SUPPRESS)  # oracle: CPU test of the launcher/exchange only
     return ap.parse_args()
+
+
+CPU_SAMPLE = 1024  # queries (ids 0..CPU_SAMPLE-1) of the CPU legs: cpu_baseline and --impl reference
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def world_info(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with "
+                         f"--nproc-per-node {args.gpus}, or without a launcher)")
+    return rank, world, local
 
 
 def measured_peak():
@@ -134,12 +167,14 @@ def ncu_traffic(workload: str):
 # ---------------------------------------------------------------- helpers
 
 def c5_config(args):
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     cfg = synth.CONFIGS["c5"]
     if args.c5_median:
         cfg = synth.replace(cfg, c5_median=args.c5_median)
     if args.c5_docs:
         cfg = synth.replace(cfg, n_docs=args.c5_docs)
+    if args.c5_block_size:
+        cfg = synth.replace(cfg, block_size=args.c5_block_size)
     if args.queries:
         cfg = synth.replace(cfg, n_queries=args.queries)
     return cfg
@@ -188,7 +223,7 @@ def workload_name(cfg):
 def build_c1_index(cfg, device):
     """Config-1 index built on the device from the seeded corpus."""
     import paper_1905_09624_b200 as cb
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     buf, off = synth.docs(cfg)
     names = synth.doc_names(cfg)
     docs = [(names[i], [buf[int(off[i]):int(off[i + 1])].tobytes()]) for i in range(cfg.n_docs)]
@@ -200,10 +235,16 @@ def build_c1_index(cfg, device):
 
 def run_reference(args):
     """The reference's own CPU query path (oracle/_ref = unmodified
-    /root/reference sources), threaded over all host cores."""
+    /root/reference sources), threaded over all host cores.  This process
+    loads nothing outside oracle/: the inputs come from the oracle library's
+    copy of the seeded generator (workloads.synth.bind), never from the
+    product package."""
     from oracle import oracle as O
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
+    O.ensure_built()
+    synth.bind(O.ORACLE_SO)
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
@@ -212,7 +253,7 @@ def run_reference(args):
         t0 = time.perf_counter()
         ref, how = open_ref_c5(cfg, cores)
         setup_s = time.perf_counter() - t0
-        per_step = args.cpu_sample or 16 * cores
+        per_step = args.cpu_sample or CPU_SAMPLE
         K = cfg.K
     else:
         cfg = synth.CONFIGS["c1"]
@@ -228,10 +269,12 @@ def run_reference(args):
         per_step = args.cpu_sample or cfg.n_queries
         K = cfg.K
         how = "the reference's open_resident of its own build"
+    # every step answers the same bounded sample: query ids 0..per_step-1, the
+    # ids the GPU arm's cpu_baseline times
+    ids = np.arange(per_step, dtype=np.uint64) % np.uint64(cfg.n_queries)
+    qb, qo = synth.queries(cfg, ids)
     times, grams = [], []
     for step in range(args.warmup + args.steps):
-        ids = (np.arange(per_step, dtype=np.uint64) + step * per_step) % cfg.n_queries
-        qb, qo = synth.queries(cfg, ids)
         t = time.perf_counter()
         ell, sk, st, nh, _ = ref.query_batch(qb, qo, K, threads=cores)
         dt = time.perf_counter() - t
@@ -240,14 +283,14 @@ def run_reference(args):
             grams.append(int(ell.sum()))
     value = sum(grams) / sum(times)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u64",
         "data": "synthetic (seeded)", "impl": "reference",
-        "config": {"workload": workload_name(cfg), "step": f"{per_step}-query bounded sample",
+        "config": {"workload": workload_name(cfg), "step": f"{per_step}-query bounded sample (ids 0..{per_step - 1})",
                    "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{per_step} queries per step x {args.steps} steps over {how}, "
+                         "sample": f"query ids 0..{per_step - 1} every step x {args.steps} steps over {how}, "
                                    f"index load {setup_s:.1f}s excluded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -259,7 +302,7 @@ def run_reference(args):
 
 def cpu_baseline_c5(cfg, sample):
     from oracle import oracle as O
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     cores = os.cpu_count() or 1
     ref, how = open_ref_c5(cfg, cores)
     qb, qo = synth.queries(cfg, np.arange(sample, dtype=np.uint64))
@@ -275,16 +318,17 @@ def cpu_baseline_c5(cfg, sample):
 def run_gpu(args):
     import torch
     import paper_1905_09624_b200 as cb
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = world_info(args)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (NVLS etc.) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.shard == "blocks":
+        return run_gpu_blocks(args, rank, world, local, dist)
 
     if args.config == "c5":
         cfg = c5_config(args)
@@ -407,7 +451,7 @@ def run_gpu(args):
         if not args.no_cpu_baseline:
             try:
                 if cfg.name == "c5":
-                    cpu_base = cpu_baseline_c5(cfg, args.cpu_sample or 2000)
+                    cpu_base = cpu_baseline_c5(cfg, args.cpu_sample or CPU_SAMPLE)
                 else:
                     cpu_base = cpu_baseline_c1(cfg)
             except Exception as e:  # report, do not die
@@ -453,7 +497,7 @@ def run_gpu(args):
 def cpu_baseline_c1(cfg):
     import tempfile
     from oracle import oracle as O
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     cores = os.cpu_count() or 1
     buf, off = synth.docs(cfg)
     names = synth.doc_names(cfg)
@@ -535,10 +579,139 @@ def bench_build_c3(cb, synth, device):
     return out
 
 
+def run_gpu_blocks(args, rank, world, local, dist):
+    """--shard blocks: the C5 index split by blocks over the ranks (an index
+    larger than one GPU, e.g. the literal-median 185 GB C5 over 2+ GPUs).
+    Every rank answers the whole batch on its blocks; one step = local
+    kernels 1-3, the hit lists to the host, the tensor all_gather of the hit
+    lists (NCCL) and the rank-0 merge by (score desc, name asc).  Strong
+    scaling: the batch and the index are fixed, N GPUs share them."""
+    import torch
+    import paper_1905_09624_b200 as cb
+    from workloads import synth
+    from paper_1905_09624_b200.dist import gather_block_hits, name_ranks, reduce_max, shard_range
+    if args.config != "c5":
+        raise SystemExit("--shard blocks serves the compact C5 index")
+    cfg = c5_config(args)
+    nb = (cfg.n_docs + cfg.block_size - 1) // cfg.block_size
+    b_lo, b_hi = shard_range(nb, rank, world)
+    t0 = time.perf_counter()
+    view = cb.synth_c5_blocks(cfg.seed, b_lo, b_hi, cfg.n_docs, cfg.block_size, cfg.c5_median,
+                              cfg.c5_sigma, cfg.p, device=local)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream(device=local)
+    view.set_stream(stream.cuda_stream)
+    off = view.column_offset()
+    nr = None
+    # names of the C5 documents are zero-padded "docNNNNNN" of their draw
+    # index; rank 0 needs every column's name rank: from the full header
+    # order (term_count, name) -- the shard views know their own names only,
+    # so gather them once (setup, untimed)
+    from paper_1905_09624_b200.dist import all_gather_arrays
+    my_names = view.doc_names()
+    codes = np.array([int(n[3:]) for n in my_names], np.int64)  # "doc%06d" -> draw index
+    parts = all_gather_arrays([codes], f"cuda:{local}")
+    if rank == 0:
+        all_codes = np.concatenate([p[0] for p in parts])
+        width = max(6, len(str(cfg.n_docs - 1)))
+        nr = name_ranks([b"doc" + str(int(c)).zfill(width).encode() for c in all_codes])
+    qb, qo = synth.queries(cfg)
+    n = len(qo) - 1
+    dev = f"cuda:{local}"
+
+    def step():
+        r = cb.query_batch_raw(view, qb, qo, cfg.K)
+        merged = gather_block_hits(r.hit_n, r.docs.astype(np.int64) + off, r.scores, nr, 0, dev)
+        return r, merged
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    outs = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t) / args.steps * 1e3
+    if dist:
+        dist.barrier()
+    ms = reduce_max(wall, dev)
+    grams = int(outs[-1][0].ell.astype(np.uint64).sum())  # every shard sees the whole batch
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": grams / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8/u64", "data": "synthetic (seeded)",
+            "config": {"workload": workload_name(cfg), "queries": n,
+                       "parallelism": f"block shards x{world} (blocks {b_lo}..{b_hi - 1} on rank 0 of {nb})",
+                       "index_bytes_hbm_rank0": view.device_bytes(), "setup_s": setup_s,
+                       "timing": "host wall clock per step (kernels + hit D2H + NCCL all_gather + merge), "
+                                 "max over ranks"},
+            "hits_total": int(outs[-1][1][0].sum()),
+        }
+        print(json.dumps(line), flush=True)
+    view.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_oracle_engine(args):
+    """Test-only (--engine oracle): the launcher, the world-size check, the
+    max-over-ranks timing and the block-shard exchange of the GPU arm, with
+    the CPU oracle answering each rank's share (gloo; no GPU).  Never a bench
+    number."""
+    import torch.distributed as tdist
+    from oracle import oracle as O
+    from workloads import synth
+    from paper_1905_09624_b200.dist import gather_block_hits, name_ranks, reduce_max, shard_range
+    rank, world, _ = world_info(args)
+    dist = None
+    if world > 1:
+        tdist.init_process_group("gloo")
+        dist = tdist
+    cfg = c5_config(args)
+    idx = O.OracleIndex.c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p)
+    names = idx.names()
+    blocks = idx.blocks()
+    b_lo, b_hi = shard_range(len(blocks), rank, world)
+    col_lo, col_hi = blocks[b_lo][2], blocks[b_hi - 1][2] + blocks[b_hi - 1][0]
+    qb, qo = synth.queries(cfg)
+    n = len(qo) - 1
+    t = time.perf_counter()
+    hn, cols, sc, grams, full = [], [], [], 0, []
+    for i in range(n):
+        ell, _, h, _ = idx.query(qb[int(qo[i]):int(qo[i + 1])].tobytes(), cfg.K)
+        grams += ell
+        full.append(h)
+        mine = [(d, s_) for d, s_ in h if col_lo <= d < col_hi] if args.shard == "blocks" else h
+        hn.append(len(mine))
+        cols += [d for d, _ in mine]
+        sc += [s_ for _, s_ in mine]
+    merged = gather_block_hits(np.asarray(hn, np.int64), np.asarray(cols, np.int64), np.asarray(sc, np.int64),
+                               name_ranks(names), 0) if args.shard == "blocks" else None
+    ms = reduce_max((time.perf_counter() - t) * 1e3)
+    if rank == 0:
+        ok = None
+        if merged is not None:
+            want = [(d, s_) for h in full for d, s_ in h]
+            ok = list(zip(merged[1].tolist(), merged[2].tolist())) == want
+        print(json.dumps({"metric": METRIC, "value": grams / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                          "steps": 1, "warmup": 0, "ms_per_step": ms, "engine": "oracle (test only)",
+                          "shard": args.shard, "hits_identical": ok}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.engine == "oracle":
+        return run_oracle_engine(args)
     return run_gpu(args)
 
 

@@ -303,6 +303,13 @@ int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size,
                             double sigma, double p, int device, cobs_gpu_index** out, char* err,
                             size_t errlen);
 
+/* Blocks [block_lo, block_hi) of the same config-5 index as a block shard
+ * (cobs_gpu_index_open_blocks semantics: hit columns are local,
+ * cobs_gpu_index_column_offset maps them to file columns). */
+int cobs_gpu_index_synth_c5_blocks(uint64_t seed, uint64_t n_docs, uint64_t block_size, double median,
+                                   double sigma, double p, uint64_t block_lo, uint64_t block_hi, int device,
+                                   cobs_gpu_index** out, char* err, size_t errlen);
+
 /* Generate documents [doc_lo, doc_hi) of a synthetic corpus on the device
  * into `dev_out` (device pointer, sum of lengths bytes, concatenated in
  * document order). alpha: 0 DNA, 1 amino acids. */

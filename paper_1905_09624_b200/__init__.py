@@ -282,6 +282,20 @@ def synth_c5(seed: int, n_docs: int = 100_000, block_size: int = 1024, median: f
     return DeviceIndexView(h.value)
 
 
+def synth_c5_blocks(seed: int, block_lo: int, block_hi: int, n_docs: int = 100_000,
+                    block_size: int = 1024, median: float = 2.4e6, sigma: float = 0.5, p: float = 0.3,
+                    device: int = 0) -> DeviceIndexView:
+    """Blocks [block_lo, block_hi) of the config-5 index as a block shard
+    (like open_blocks: hit columns are local, column_offset() maps them)."""
+    h = C.c_void_p()
+    err = _errbuf()
+    rc = N.lib.cobs_gpu_index_synth_c5_blocks(seed, n_docs, block_size, median, sigma, p, block_lo,
+                                              block_hi, device, C.byref(h), err, len(err))
+    if rc:
+        _raise(rc, err)
+    return DeviceIndexView(h.value)
+
+
 def write_index(view: DeviceIndexView, path: str) -> None:
     """cobs::write_index(const IndexView&, path) (storage.hpp:14)."""
     err = _errbuf()

@@ -106,6 +106,9 @@ SIGNATURES = {
     "cobs_gpu_index_synth_c5": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                           C.c_double, C.c_double, C.c_int, C.POINTER(vp),
                                           C.c_char_p, C.c_size_t]),
+    "cobs_gpu_index_synth_c5_blocks": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                                 C.c_double, C.c_double, C.c_uint64, C.c_uint64,
+                                                 C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "cobs_gpu_index_open_file": (C.c_int, [C.c_char_p, C.c_int, C.c_uint64, C.POINTER(vp), C.c_char_p,
                                            C.c_size_t]),
     "cobs_gpu_index_open_blocks": (C.c_int, [C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(vp),

@@ -450,6 +450,17 @@ int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size,
     });
 }
 
+int cobs_gpu_index_synth_c5_blocks(uint64_t seed, uint64_t n_docs, uint64_t block_size, double median,
+                                   double sigma, double p, uint64_t block_lo, uint64_t block_hi, int device,
+                                   cobs_gpu_index** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        auto h = std::make_unique<cobs_gpu_index>();
+        h->ix = cobsg::synth_c5_index(seed, n_docs, block_size, median, sigma, p, device, block_lo, block_hi);
+        *out = h.release();
+    });
+}
+
 int cobs_gpu_synth_docs(uint64_t seed, int alpha, const uint64_t* doc_len, uint64_t doc_lo,
                         uint64_t doc_hi, uint8_t* dev_out, int device) {
     return guarded(nullptr, 0, [&] { cobsg::synth_docs(seed, alpha, doc_len, doc_lo, doc_hi, dev_out, device); });

@@ -512,8 +512,14 @@ __global__ void c5_fill_kernel(uint32_t* rows, uint64_t words, uint32_t words_pe
 }
 
 std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n, uint64_t B, double median,
-                                            double sigma, double p, int device) {
+                                            double sigma, double p, int device, uint64_t block_lo,
+                                            uint64_t block_hi) {
     if (n == 0 || B == 0) throw UsageError("synth_c5: n_docs and block_size must be >= 1");
+    const uint64_t nb_all = (n + B - 1) / B;
+    if (block_hi > nb_all) block_hi = nb_all;
+    if (!(block_lo < block_hi))
+        throw UsageError("synth_c5: block range [" + std::to_string(block_lo) + ", " + std::to_string(block_hi) +
+                         ") outside [0, " + std::to_string(nb_all) + ")");
     auto ix = std::make_unique<DeviceIndex>();
     ix->device = device;
     IndexMeta& m = ix->meta;
@@ -538,10 +544,12 @@ std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n, uint64_t 
         if (tc[a] != tc[b]) return tc[a] < tc[b];
         return names[a] < names[b];
     });
-    uint64_t nb = (n + B - 1) / B;
+    // blocks [block_lo, block_hi) only: a block shard of the same index
+    // (open_index_blocks semantics; column_offset maps its columns)
+    const uint64_t nb = block_hi - block_lo;
     std::vector<uint32_t> thr(nb);
     for (uint64_t b = 0; b < nb; ++b) {
-        uint64_t lo = b * B, hi = std::min(n, lo + B), mx = 0;
+        uint64_t lo = (block_lo + b) * B, hi = std::min(n, lo + B), mx = 0;
         BlockMeta bm;
         bm.doc_count = hi - lo;
         for (uint64_t i = lo; i < hi; ++i) {
@@ -553,13 +561,14 @@ std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n, uint64_t 
         m.blocks.push_back(bm);
     }
     m.layout();
+    ix->column_offset = block_lo * B;
     ix->allocate();
     for (uint64_t b = 0; b < nb; ++b) {
         const DevBlock& d = ix->blocks[b];
         uint64_t words = d.w * (d.pitch / 4);
         c5_fill_kernel<<<148 * 16, 256, 0, ix->stream>>>(
             reinterpret_cast<uint32_t*>(ix->payload + d.base), words, d.pitch / 4,
-            syn_c5_key(seed, b), thr[b], d.dc);
+            syn_c5_key(seed, block_lo + b), thr[b], d.dc);
         COBS_CUDA(cudaGetLastError());
     }
     ix->finish_upload();

@@ -148,7 +148,8 @@ std::unique_ptr<DeviceIndex> open_index_blocks(const ByteSource& src, int device
                                                uint64_t block_hi);
 // Config-5 procedural index generated in HBM.
 std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n_docs, uint64_t block_size,
-                                            double median, double sigma, double p, int device);
+                                            double median, double sigma, double p, int device,
+                                            uint64_t block_lo = 0, uint64_t block_hi = ~0ull);
 
 struct QueryResults {
     uint64_t n = 0;

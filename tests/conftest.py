@@ -14,7 +14,7 @@ def pytest_configure(config):
 
 def _ensure_built():
     lib = os.path.join(ROOT, "paper_1905_09624_b200", "_lib", "libcobs_gpu.so")
-    synth = os.path.join(ROOT, "paper_1905_09624_b200", "_lib", "libcobs_synth.so")
+    synth = os.path.join(ROOT, "workloads", "_lib", "libcobs_synth.so")
     orc = os.path.join(ROOT, "oracle", "_build", "libcobs_oracle.so")
     if not (os.path.exists(lib) and os.path.exists(synth)):
         subprocess.run(["make", "-C", ROOT, "-j8", "lib"], check=True)

@@ -83,26 +83,27 @@ def test_two_rank_gather_equals_single_rank():
     assert list(merged["docs"]) == want_docs
 
 
-def _shard_payload(idx, names, pats, K, top_t, col_lo, col_hi):
-    """A block shard's answer, computed from the oracle's full-index hits
-    restricted to the shard's columns (what the shard's own engine returns)."""
-    out = {"ell": [], "status": [], "hits": []}
+def _shard_hits(idx, pats, K, top_t, col_lo, col_hi):
+    """A block shard's answer (hit_n, global columns, scores), computed from
+    the oracle's full-index hits restricted to the shard's columns and cut
+    to top_t (what the shard's own engine returns)."""
+    names = idx.names()
+    hn, cols, scores = [], [], []
     for p in pats:
         e, s, h, _ = idx.query(p, K)
-        mine = [(d, sc, names[d]) for d, sc in h if col_lo <= d < col_hi]
-        mine.sort(key=lambda x: (-x[1], x[2]))
-        out["ell"].append(e)
-        out["status"].append(0)
-        out["hits"].append(mine[:top_t] if top_t else mine)
-    out["ell"] = np.asarray(out["ell"], np.uint64)
-    out["status"] = np.asarray(out["status"], np.int32)
-    return out
+        mine = [(d, sc) for d, sc in h if col_lo <= d < col_hi]
+        mine.sort(key=lambda x: (-x[1], names[x[0]]))
+        mine = mine[:top_t] if top_t else mine
+        hn.append(len(mine))
+        cols += [d for d, _ in mine]
+        scores += [sc for _, sc in mine]
+    return np.asarray(hn, np.int64), np.asarray(cols, np.int64), np.asarray(scores, np.int64)
 
 
 def _block_worker(rank, world, port, img, pats, top_t, q):
     import torch.distributed as dist
     from oracle import oracle as O
-    from paper_1905_09624_b200.dist import gather_block_shards, shard_range
+    from paper_1905_09624_b200.dist import gather_block_hits, name_ranks, shard_range
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -111,17 +112,18 @@ def _block_worker(rank, world, port, img, pats, top_t, q):
     b_lo, b_hi = shard_range(len(blocks), rank, world)
     col_lo = blocks[b_lo][2]
     col_hi = blocks[b_hi - 1][2] + blocks[b_hi - 1][0]
-    payload = _shard_payload(idx, idx.names(), pats, 0.3, top_t, col_lo, col_hi)
-    merged = gather_block_shards(payload, top_t)
+    hn, cols, sc = _shard_hits(idx, pats, 0.3, top_t, col_lo, col_hi)
+    merged = gather_block_hits(hn, cols, sc, name_ranks(idx.names()), top_t)
     if rank == 0:
         q.put(merged)
     dist.destroy_process_group()
 
 
 def test_two_rank_block_shards_equal_unsharded():
-    """Block sharding's one exchange: rank r holds blocks shard_range(nb, r, 2)
-    of a compact index; the rank-0 merge of the shard hit lists by (score
-    desc, name asc), cut to top_t, equals querying the whole index."""
+    """Block sharding's one exchange (tensor all_gather, gloo here, NCCL on
+    GPUs): rank r holds blocks shard_range(nb, r, 2) of a compact index; the
+    rank-0 merge of the shard hit lists by (score desc, name asc), cut to
+    top_t, equals querying the whole index."""
     from oracle import oracle as O
     rng = random.Random(8)
     docs = [(b"d%03d" % rng.randrange(1000), [bytes(rng.choice(b"ACGT") for _ in range(rng.randint(60, 700)))])
@@ -130,14 +132,15 @@ def test_two_rank_block_shards_equal_unsharded():
     img = O.build_image(docs, block_size=6, kind=1)
     pats = [docs[i % len(docs)][1][0][:70 + 7 * i] for i in range(10)] + [b"ACGT" * 30]
     idx = O.OracleIndex.parse(img)
-    names = idx.names()
     for top_t in (0, 3):
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
         mp.start_processes(_block_worker, args=(2, _free_port(), img, pats, top_t, q), nprocs=2, join=True,
                            start_method="spawn")
-        merged = q.get(timeout=60)
+        hn, cols, sc = q.get(timeout=60)
+        o = 0
         for i, p in enumerate(pats):
             _, _, want, _ = idx.query(p, 0.3, top_t)
-            assert [(d, sc) for d, sc, _ in merged[i]] == want, (top_t, i)
-            assert all(names[d] == nm for d, _, nm in merged[i])
+            got = list(zip(cols[o:o + hn[i]].tolist(), sc[o:o + hn[i]].tolist()))
+            o += int(hn[i])
+            assert got == want, (top_t, i)

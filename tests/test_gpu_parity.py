@@ -187,7 +187,7 @@ def test_c5_procedural_small(gpu):
     """Config-5 generator: device rows == host rows; header == oracle's
     (and hence the reference writer's, test_oracle_vs_ref.py); scores == the
     oracle over the procedural view."""
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     seed, n, B, med, sig, p = 7, 3000, 1024, 4000.0, 0.5, 0.3
     view = cb.synth_c5(seed, n, B, med, sig, p, device=gpu)
     orc = O.OracleIndex.c5(seed, n, B, med, sig, p)
@@ -213,7 +213,7 @@ def test_build_device_resident(gpu):
     """cobs_gpu_build_ex: device-resident sequences in, queryable index out;
     its image equals the host-input build's and the oracle's."""
     import torch
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     cfg = synth.scaled(synth.CONFIGS["c3"], 150, len_scale=0.001, n_queries=20, block_size=32)
     lengths = synth.doc_lengths(cfg)
     dev = torch.empty(int(lengths.sum()), dtype=torch.uint8, device="cuda")
@@ -294,7 +294,7 @@ def test_host_resident_streaming(gpu, tmp_path, kind, frac, from_file):
     buffers (slabs of a block's slices, several blocks per group); results are
     identical to the resident index and the oracle; every batch copies the
     whole payload once."""
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     cfg = synth.scaled(synth.CONFIGS["c2"], 3000 if kind == 0 else 2600, len_scale=0.001,
                        n_queries=60, kind=kind, block_size=256, k=2)
     docs = [(n, [s]) for n, s in zip(synth.doc_names(cfg), _doc_bytes(cfg))]
@@ -332,7 +332,7 @@ def test_host_resident_streaming(gpu, tmp_path, kind, frac, from_file):
 
 
 def _doc_bytes(cfg):
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     buf, off = synth.docs(cfg)
     return [buf[int(off[i]):int(off[i + 1])].tobytes() for i in range(cfg.n_docs)]
 
@@ -346,7 +346,7 @@ def test_streaming_budget_too_small(gpu, tmp_path):
 def test_threshold_pruning_same_hits(gpu):
     """COBS_Q_PRUNE (stop reading a slice's rows once no document can reach
     tau) returns exactly the unpruned hit lists (which equal the oracle's)."""
-    from paper_1905_09624_b200 import synth
+    from workloads import synth
     for cfg in (synth.scaled(synth.CONFIGS["c1"], 300, len_scale=0.05, n_queries=300),
                 synth.scaled(synth.CONFIGS["c2"], 400, len_scale=0.005, n_queries=200)):
         docs = [(n, [s]) for n, s in zip(synth.doc_names(cfg), _doc_bytes(cfg))]
@@ -534,11 +534,11 @@ def test_block_shards(gpu, tmp_path):
     for K, top_t in ((0.3, 0), (0.3, 4), (1e-12, 0), (0.9, 1)):
         want = cb.query_batch(full, pats, K, top_t, scores=(top_t == 0))
         parts = [cb.query_batch(s, pats, K, top_t, scores=(top_t == 0)) for s in shards]
-        merged = D.merge_block_shards([D.shard_hits(r, s.doc_names(), s.column_offset())
-                                       for r, s in zip(parts, shards)], top_t)
+        hn, cols, sc = D.merge_hits([(r.hit_n, r.docs.astype(np.int64) + s.column_offset(), r.scores)
+                                     for r, s in zip(parts, shards)], D.name_ranks(full.doc_names()), top_t)
+        assert np.array_equal(hn, want.hit_n.astype(np.int64)), (K, top_t)
+        assert np.array_equal(cols, want.docs.astype(np.int64)) and np.array_equal(sc, want.scores.astype(np.int64))
         for i in range(len(pats)):
-            d, sc = want.hits(i)
-            assert [(a, b) for a, b, _ in merged[i]] == [(int(x), int(y)) for x, y in zip(d, sc)], (K, top_t, i)
             for r in parts:
                 assert r.ell[i] == want.ell[i] and r.status[i] == want.status[i]
         if top_t == 0:
@@ -653,3 +653,37 @@ def test_row_bytes_equal_reference_bytes_read(gpu, tmp_path):
         got = cb.query_batch(view, pats, 0.5)
         assert got.row_bytes == ra.bytes_read(), (k, kind)
         view.close()
+
+
+def test_synth_c5_block_shards(gpu):
+    """bench.py --shard blocks: block shards of the procedural config-5 index
+    (synth_c5_blocks) hold exactly the full index's blocks, and their merged
+    hit lists equal the unsharded index's (small instance)."""
+    from paper_1905_09624_b200 import dist as D
+    from workloads import synth
+    cfg = synth.replace(synth.CONFIGS["c5"], n_docs=3000, block_size=256, c5_median=2e4, n_queries=64)
+    args = (cfg.seed,)
+    kw = dict(n_docs=cfg.n_docs, block_size=cfg.block_size, median=cfg.c5_median, sigma=cfg.c5_sigma, p=cfg.p)
+    full = cb.synth_c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p, device=gpu)
+    nb = full.block_count()
+    cuts = [0, 3, 7, nb]
+    shards = [cb.synth_c5_blocks(*args, a, b, device=gpu, **kw) for a, b in zip(cuts, cuts[1:])]
+    assert [s.column_offset() for s in shards] == [c * cfg.block_size for c in cuts[:-1]]
+    for s, a in zip(shards, cuts):
+        for b in range(s.block_count()):
+            assert s.width(b) == full.width(a + b)
+            for r in (0, s.width(b) // 2, s.width(b) - 1):
+                assert s.row_data(b, r) == full.row_data(a + b, r)
+    qb, qo = synth.queries(cfg)
+    # random queries score only false positives (density ~0.3 per row), so
+    # K around 0.3 gives a mix of hits and misses
+    for K, top_t in ((0.3, 0), (0.32, 5), (1e-12, 3)):
+        want = cb.query_batch_raw(full, qb, qo, K, top_t)
+        parts = [cb.query_batch_raw(s, qb, qo, K, top_t) for s in shards]
+        hn, cols, sc = D.merge_hits([(r.hit_n, r.docs.astype(np.int64) + s.column_offset(), r.scores)
+                                     for r, s in zip(parts, shards)], D.name_ranks(full.doc_names()), top_t)
+        assert np.array_equal(hn, want.hit_n.astype(np.int64)), (K, top_t)
+        assert np.array_equal(cols, want.docs.astype(np.int64)) and np.array_equal(sc, want.scores.astype(np.int64))
+        assert int(want.hit_n.sum()) > 0
+    for v in shards + [full]:
+        v.close()

@@ -12,7 +12,7 @@ import pytest
 
 import paper_1905_09624_b200 as cb
 from oracle import oracle as O
-from paper_1905_09624_b200 import synth
+from workloads import synth
 
 pytestmark = pytest.mark.gpu
 

@@ -4,7 +4,7 @@ import sys, time
 sys.path.insert(0, '.')
 import numpy as np
 import paper_1905_09624_b200 as cb
-from paper_1905_09624_b200 import synth
+from workloads import synth
 name = sys.argv[1] if len(sys.argv) > 1 else "c1"
 cfg = synth.CONFIGS["c1"] if name == "c1" else synth.scaled(synth.CONFIGS["c2"], 2000)
 buf, off = synth.docs(cfg)

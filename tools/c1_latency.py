@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 import numpy as np
 import torch
 import paper_1905_09624_b200 as cb
-from paper_1905_09624_b200 import synth
+from workloads import synth
 cfg = synth.CONFIGS["c1"]
 buf, off = synth.docs(cfg)
 names = synth.doc_names(cfg)

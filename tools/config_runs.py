@@ -29,7 +29,7 @@ import torch  # noqa: E402
 
 import paper_1905_09624_b200 as cb  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from paper_1905_09624_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 
 
 def column_bits(img: bytes, idx: O.OracleIndex, block: int, col: int) -> np.ndarray:

@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 import paper_1905_09624_b200 as cb  # noqa: E402
-from paper_1905_09624_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 
 
 def main():

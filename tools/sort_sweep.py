@@ -5,7 +5,7 @@
 import json, os, sys
 sys.path.insert(0, '.')
 import paper_1905_09624_b200 as cb
-from paper_1905_09624_b200 import synth
+from workloads import synth
 docs = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 view = cb.synth_c5(1905_09624, docs, 1024, 2.4e6, 0.5, 0.3, device=0)

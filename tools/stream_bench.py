@@ -19,7 +19,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1905_09624_b200 as cb  # noqa: E402
-from paper_1905_09624_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 
 
 def main():

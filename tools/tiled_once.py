@@ -2,7 +2,7 @@
 import os, sys
 sys.path.insert(0, '.')
 import paper_1905_09624_b200 as cb
-from paper_1905_09624_b200 import synth
+from workloads import synth
 docs = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 26000
 median = float(sys.argv[3]) if len(sys.argv) > 3 else 2.4e6

@@ -3,7 +3,7 @@ import json, os, sys, time
 sys.path.insert(0, '.')
 import numpy as np
 import paper_1905_09624_b200 as cb
-from paper_1905_09624_b200 import synth
+from workloads import synth
 docs = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 26000
 view = cb.synth_c5(7, docs, 1024, 2.4e6, 0.5, 0.3, device=0)

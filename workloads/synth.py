@@ -1,7 +1,8 @@
 """Seeded synthetic workloads for the five BASELINE.json configs.
 
-Input generation only (csrc/synth.h through _lib/libcobs_synth.so); the same
-header drives the device generators, so host and device see identical bytes.
+Input generation only (paper_1905_09624_b200/csrc/synth.h through
+workloads/_lib/libcobs_synth.so); the same header drives the device
+generators, so host and device see identical bytes.
 No public dataset is used: the paper's 100k-sample McCortex corpus and its
 query sets are absent, and these seeded inputs take their shapes instead
 (DESIGN.md §7).
@@ -17,9 +18,34 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "_lib", "libcobs_synth.so")
-if not os.path.exists(_SO):
-    raise ImportError(f"{_SO} missing: run `make lib`")
-_lib = C.CDLL(_SO)
+
+
+class _Lib:
+    """The generator's C ABI (workloads/synth_host.c over csrc/synth.h),
+    bound on first use.  `bind(path)` selects another build of the same
+    functions: bench.py's reference arm binds the oracle library's copy so
+    that process loads nothing outside oracle/ (no product code)."""
+    def __init__(self):
+        self.h = None
+
+    def bind(self, path: str) -> None:
+        h = C.CDLL(path)
+        _declare(h)
+        self.h = h
+
+    def __getattr__(self, name):
+        if self.h is None:
+            if not os.path.exists(_SO):
+                raise ImportError(f"{_SO} missing: run `make lib`")
+            self.bind(_SO)
+        return getattr(self.h, name)
+
+
+_lib = _Lib()
+
+
+def bind(path: str) -> None:
+    _lib.bind(path)
 
 DNA, AA = 0, 1
 Q_RANDOM, Q_SUBST, Q_INDEL = 0, 1, 2
@@ -32,18 +58,18 @@ class QuerySpecC(C.Structure):
                 ("mixed", C.c_int)]
 
 
-_u64p = C.POINTER(C.c_uint64)
-_lib.syn_c_doc_lengths.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,
-                                   C.c_uint64, C.c_void_p]
-_lib.syn_c_c5_term_counts.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_void_p]
-_lib.syn_c_c5_thr16.argtypes = [C.c_uint64, C.c_uint64]
-_lib.syn_c_c5_thr16.restype = C.c_uint32
-_lib.syn_c_c5_row.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
-                              C.c_uint64, C.c_void_p]
-_lib.syn_c_docs.argtypes = [C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
-                            C.c_int]
-_lib.syn_c_queries.argtypes = [C.POINTER(QuerySpecC), C.c_void_p, C.c_uint64, C.c_void_p,
-                               C.c_uint64, C.c_void_p, C.c_int]
+def _declare(h) -> None:
+    h.syn_c_doc_lengths.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                                    C.c_uint64, C.c_void_p]
+    h.syn_c_c5_term_counts.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_void_p]
+    h.syn_c_c5_thr16.argtypes = [C.c_uint64, C.c_uint64]
+    h.syn_c_c5_thr16.restype = C.c_uint32
+    h.syn_c_c5_row.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                               C.c_uint64, C.c_void_p]
+    h.syn_c_docs.argtypes = [C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                             C.c_int]
+    h.syn_c_queries.argtypes = [C.POINTER(QuerySpecC), C.c_void_p, C.c_uint64, C.c_void_p,
+                                C.c_uint64, C.c_void_p, C.c_int]
 
 
 @dataclass(frozen=True)

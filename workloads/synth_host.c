@@ -5,7 +5,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "synth.h"
+#include "../paper_1905_09624_b200/csrc/synth.h"
 
 void syn_c_doc_lengths(uint64_t seed, uint64_t n, int dist, double a, double b, uint64_t minlen,
                        uint64_t* out) {
