@@ -589,7 +589,7 @@ def run_gpu_blocks(args, rank, world, local, dist):
     import torch
     import paper_1905_09624_b200 as cb
     from workloads import synth
-    from paper_1905_09624_b200.dist import gather_block_hits, name_ranks, reduce_max, shard_range
+    from paper_1905_09624_b200.dist import flat_hits, gather_block_hits, name_ranks, reduce_max, shard_range
     if args.config != "c5":
         raise SystemExit("--shard blocks serves the compact C5 index")
     cfg = c5_config(args)
@@ -621,7 +621,8 @@ def run_gpu_blocks(args, rank, world, local, dist):
 
     def step():
         r = cb.query_batch_raw(view, qb, qo, cfg.K)
-        merged = gather_block_hits(r.hit_n, r.docs.astype(np.int64) + off, r.scores, nr, 0, dev)
+        hn, cols, sc = flat_hits(r)
+        merged = gather_block_hits(hn, cols + off, sc, nr, 0, dev)
         return r, merged
 
     for _ in range(args.warmup):

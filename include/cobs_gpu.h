@@ -142,6 +142,13 @@ int cobs_gpu_index_write(const cobs_gpu_index* index, const char* path, char* er
 int cobs_gpu_index_image(const cobs_gpu_index* index, uint8_t** image, uint64_t* image_len, char* err,
                          size_t errlen);
 
+/* The same image written into a caller buffer (no library allocation, no
+ * intermediate copy: for images of tens of GB).  *image_len receives the
+ * size; with dst == NULL or cap < size nothing is written and 1 returned
+ * (query the size with dst == NULL). */
+int cobs_gpu_index_image_into(const cobs_gpu_index* index, uint8_t* dst, uint64_t cap, uint64_t* image_len,
+                              char* err, size_t errlen);
+
 /* ---- batch query ------------------------------------------------------ */
 
 /* flags */

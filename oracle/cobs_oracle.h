@@ -111,6 +111,34 @@ int orc_c5_make(uint64_t seed, uint64_t n_docs, uint64_t block_size, double medi
  * proj/src/storage.cpp:345-380 writes them. */
 int orc_header_image(const orc_index* idx, uint8_t** img, uint64_t* len);
 
+/* Full-size streaming check (oracle/cobs_stream.c): the index image `img`
+ * of the seeded synthetic corpus (synth.h documents 0..n_docs-1, lengths
+ * doc_len[], names "doc" + zero-padded draw index) against the build the
+ * reference would make of it -- every payload byte and the whole header --
+ * without materialising the corpus or a second index.  Returns 0 (report
+ * filled), 1 unsupported shape, 2 image unparsable, 3 documents/names do not
+ * match the corpus, 4 out of memory. */
+typedef struct orc_stream_spec {
+    uint64_t seed;
+    int alpha; /* 0 DNA, 1 the 20-letter amino-acid alphabet */
+    uint64_t n_docs;
+    const uint64_t* doc_len;
+    orc_params params;
+    int kind; /* 0 classic, 1 compact */
+} orc_stream_spec;
+
+typedef struct orc_stream_report {
+    int header_equal;            /* oracle header == image header, and lengths agree */
+    uint64_t header_len, image_len_expected;
+    uint64_t term_count_mismatch; /* documents whose term_count differs from the image's */
+    uint64_t payload_bad_bytes;   /* payload bytes that differ */
+    uint64_t bad_block, bad_row, bad_byte; /* the first (lowest) differing payload byte */
+    uint64_t windows;
+} orc_stream_report;
+
+int orc_stream_check(const orc_stream_spec* spec, const uint8_t* img, uint64_t img_len, int threads,
+                     orc_stream_report* rep, uint64_t* term_counts, char* err, size_t errlen);
+
 void orc_free(void* p);
 
 #ifdef __cplusplus

@@ -50,6 +50,18 @@ class OrcIndex(C.Structure):
                 ("c5_thr16", C.POINTER(C.c_uint32))]
 
 
+class OrcStreamSpec(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("alpha", C.c_int), ("n_docs", C.c_uint64), ("doc_len", C.c_void_p),
+                ("params", OrcParams), ("kind", C.c_int)]
+
+
+class OrcStreamReport(C.Structure):
+    _fields_ = [("header_equal", C.c_int), ("header_len", C.c_uint64), ("image_len_expected", C.c_uint64),
+                ("term_count_mismatch", C.c_uint64), ("payload_bad_bytes", C.c_uint64),
+                ("bad_block", C.c_uint64), ("bad_row", C.c_uint64), ("bad_byte", C.c_uint64),
+                ("windows", C.c_uint64)]
+
+
 class OrcHit(C.Structure):
     _fields_ = [("doc", C.c_uint64), ("score", C.c_uint64)]
 
@@ -89,6 +101,8 @@ def _load_oracle():
     L.orc_c5_make.argtypes = [_u64, _u64, _u64, C.c_double, C.c_double, C.c_double,
                               C.POINTER(OrcIndex)]
     L.orc_header_image.argtypes = [C.POINTER(OrcIndex), C.POINTER(_vp), C.POINTER(_u64)]
+    L.orc_stream_check.argtypes = [C.POINTER(OrcStreamSpec), _vp, _u64, C.c_int, C.POINTER(OrcStreamReport),
+                                   _vp, C.c_char_p, C.c_size_t]
     L.orc_free.argtypes = [_vp]
     return L
 
@@ -154,6 +168,18 @@ class OracleIndex:
         o._img = np.frombuffer(image, dtype=np.uint8).copy()
         err = C.create_string_buffer(1024)
         rc = orc().orc_parse(o._img.ctypes.data, len(image), path.encode(), C.byref(o.x), err, 1024)
+        if rc:
+            o.x = OrcIndex()
+            raise OracleError(rc, err.value.decode())
+        return o
+
+    @classmethod
+    def parse_array(cls, image: np.ndarray, path: str = "<memory>") -> "OracleIndex":
+        """parse() over a uint8 array without copying it (full-size images)."""
+        o = cls()
+        o._img = np.ascontiguousarray(image, dtype=np.uint8)
+        err = C.create_string_buffer(1024)
+        rc = orc().orc_parse(o._img.ctypes.data, len(o._img), path.encode(), C.byref(o.x), err, 1024)
         if rc:
             o.x = OrcIndex()
             raise OracleError(rc, err.value.decode())
@@ -258,6 +284,31 @@ def build_image(docs: Sequence[Tuple[bytes, Sequence[bytes]]], q=31, k=1, p=0.3,
         raise OracleError(rc, err.value.decode())
     out = _take(img, n.value)
     orc().orc_free(img)
+    return out
+
+
+def stream_check(seed: int, alpha: int, doc_len: np.ndarray, image, q=31, k=1, p=0.3, canonical=False,
+                 block_size=1024, kind=0, threads: int = 0) -> dict:
+    """orc_stream_check (oracle/cobs_stream.c): the index image (bytes or a
+    uint8 array) of the seeded synthetic corpus against the build the
+    reference would make of it, every payload byte and the whole header,
+    streamed one 64-document column group at a time.  Returns the report
+    plus the oracle's term counts by draw index."""
+    arr = np.frombuffer(image, np.uint8) if isinstance(image, (bytes, bytearray)) else image
+    arr = np.ascontiguousarray(arr, dtype=np.uint8)
+    lens = np.ascontiguousarray(doc_len, dtype=np.uint64)
+    spec = OrcStreamSpec(seed, alpha, len(lens), lens.ctypes.data,
+                         OrcParams(q, k, p, 1 if canonical else 0, block_size, 0), kind)
+    rep = OrcStreamReport()
+    tc = np.zeros(len(lens), np.uint64)
+    err = C.create_string_buffer(512)
+    rc = orc().orc_stream_check(C.byref(spec), arr.ctypes.data, len(arr), threads or (os.cpu_count() or 1),
+                                C.byref(rep), tc.ctypes.data, err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    out = {f: getattr(rep, f) for f, _ in OrcStreamReport._fields_}
+    out["header_equal"] = bool(out["header_equal"])
+    out["term_counts"] = tc
     return out
 
 

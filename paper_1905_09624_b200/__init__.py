@@ -318,6 +318,19 @@ def index_image(view: DeviceIndexView) -> bytes:
         N.lib.cobs_gpu_free(img)
 
 
+def index_image_array(view: DeviceIndexView) -> np.ndarray:
+    """index_image into one uint8 array (no intermediate copies: images of
+    tens of GB)."""
+    ln = C.c_uint64()
+    err = _errbuf()
+    N.lib.cobs_gpu_index_image_into(view._h, None, 0, C.byref(ln), err, len(err))
+    out = np.empty(ln.value, dtype=np.uint8)
+    rc = N.lib.cobs_gpu_index_image_into(view._h, out.ctypes.data, ln.value, None, err, len(err))
+    if rc:
+        _raise(rc, err)
+    return out
+
+
 def pack_patterns(patterns: Sequence[bytes]) -> Tuple[np.ndarray, np.ndarray]:
     """Concatenate patterns into (bytes, offsets[n+1])."""
     lens = np.fromiter((len(p) for p in patterns), dtype=np.uint64, count=len(patterns))

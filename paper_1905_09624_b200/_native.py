@@ -65,6 +65,8 @@ SIGNATURES = {
     "cobs_gpu_index_device_bytes": (C.c_uint64, [vp]),
     "cobs_gpu_index_row": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
     "cobs_gpu_index_write": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_size_t]),
+    "cobs_gpu_index_image_into": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p,
+                                            C.c_size_t]),
     "cobs_gpu_index_image": (C.c_int, [vp, C.POINTER(vp), C.POINTER(C.c_uint64), C.c_char_p,
                                        C.c_size_t]),
     "cobs_gpu_query_batch": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_double, C.c_uint64, C.c_uint32,

@@ -252,6 +252,17 @@ int cobs_gpu_index_image(const cobs_gpu_index* index, uint8_t** image, uint64_t*
     });
 }
 
+int cobs_gpu_index_image_into(const cobs_gpu_index* index, uint8_t* dst, uint64_t cap, uint64_t* image_len,
+                              char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const uint64_t size = cobsg::index_image_size(*index->ix);
+        if (image_len) *image_len = size;
+        if (!dst || cap < size) throw cobsg::UsageError("index_image_into: buffer of " + std::to_string(cap) +
+                                                        " bytes, image needs " + std::to_string(size));
+        cobsg::index_image_into(*index->ix, dst);
+    });
+}
+
 int cobs_gpu_query_batch(cobs_gpu_index* index, const uint8_t* patterns, const uint64_t* offsets,
                          uint64_t n, double K, uint64_t top_t, uint32_t flags, cobs_gpu_results** out,
                          char* err, size_t errlen) {

@@ -132,6 +132,18 @@ def merge_hits(parts: Sequence[Tuple[np.ndarray, np.ndarray, np.ndarray]], name_
     return hit_n, cols, sc
 
 
+def flat_hits(res) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """A batch result's hit lists as (hit_n, columns, scores), query-major
+    (each query's top_t-cut slice [hit_off, hit_off + hit_n) of its arrays)."""
+    hn = np.asarray(res.hit_n, np.int64)
+    off = np.asarray(res.hit_off, np.int64)
+    if hn.sum() == 0:
+        return hn, np.zeros(0, np.int64), np.zeros(0, np.int64)
+    starts = np.repeat(off - np.concatenate([[0], np.cumsum(hn)[:-1]]), hn)
+    idx = np.arange(int(hn.sum()), dtype=np.int64) + starts
+    return hn, np.asarray(res.docs, np.int64)[idx], np.asarray(res.scores, np.int64)[idx]
+
+
 def gather_block_hits(hit_n: np.ndarray, cols: np.ndarray, scores: np.ndarray, name_rank: np.ndarray,
                       top_t: int = 0, device="cpu") -> Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]]:
     """Block sharding's one exchange: this rank's hit lists of the whole

@@ -534,10 +534,12 @@ def test_block_shards(gpu, tmp_path):
     for K, top_t in ((0.3, 0), (0.3, 4), (1e-12, 0), (0.9, 1)):
         want = cb.query_batch(full, pats, K, top_t, scores=(top_t == 0))
         parts = [cb.query_batch(s, pats, K, top_t, scores=(top_t == 0)) for s in shards]
-        hn, cols, sc = D.merge_hits([(r.hit_n, r.docs.astype(np.int64) + s.column_offset(), r.scores)
-                                     for r, s in zip(parts, shards)], D.name_ranks(full.doc_names()), top_t)
-        assert np.array_equal(hn, want.hit_n.astype(np.int64)), (K, top_t)
-        assert np.array_equal(cols, want.docs.astype(np.int64)) and np.array_equal(sc, want.scores.astype(np.int64))
+        flat = [D.flat_hits(r) for r in parts]
+        hn, cols, sc = D.merge_hits([(h, c + s.column_offset(), x) for (h, c, x), s in zip(flat, shards)],
+                                    D.name_ranks(full.doc_names()), top_t)
+        w_hn, w_cols, w_sc = D.flat_hits(want)
+        assert np.array_equal(hn, w_hn), (K, top_t)
+        assert np.array_equal(cols, w_cols) and np.array_equal(sc, w_sc)
         for i in range(len(pats)):
             for r in parts:
                 assert r.ell[i] == want.ell[i] and r.status[i] == want.status[i]
@@ -680,10 +682,12 @@ def test_synth_c5_block_shards(gpu):
     for K, top_t in ((0.3, 0), (0.32, 5), (1e-12, 3)):
         want = cb.query_batch_raw(full, qb, qo, K, top_t)
         parts = [cb.query_batch_raw(s, qb, qo, K, top_t) for s in shards]
-        hn, cols, sc = D.merge_hits([(r.hit_n, r.docs.astype(np.int64) + s.column_offset(), r.scores)
-                                     for r, s in zip(parts, shards)], D.name_ranks(full.doc_names()), top_t)
-        assert np.array_equal(hn, want.hit_n.astype(np.int64)), (K, top_t)
-        assert np.array_equal(cols, want.docs.astype(np.int64)) and np.array_equal(sc, want.scores.astype(np.int64))
+        flat = [D.flat_hits(r) for r in parts]
+        hn, cols, sc = D.merge_hits([(h, c + s.column_offset(), x) for (h, c, x), s in zip(flat, shards)],
+                                    D.name_ranks(full.doc_names()), top_t)
+        w_hn, w_cols, w_sc = D.flat_hits(want)
+        assert np.array_equal(hn, w_hn), (K, top_t)
+        assert np.array_equal(cols, w_cols) and np.array_equal(sc, w_sc)
         assert int(want.hit_n.sum()) > 0
     for v in shards + [full]:
         v.close()

@@ -1,16 +1,16 @@
 #!/usr/bin/env python
 """Full-size runs of BASELINE.json configs 1-4 on one B200: build the index
 on the device from the seeded corpus (documents generated in HBM), query the
-config's batch, and check parity against the CPU oracle through properties
-that do not need an oracle-sized build:
+config's whole batch, and check parity with the CPU oracle:
 
-  * header: widths == size_filter(block max term_count) (oracle's sizing),
-    compact order (term_count, name) non-decreasing;
-  * sampled documents: term_count == the oracle's extract_terms, and the
-    document's whole bit column == the oracle's single-document build with the
-    same forced width (every row, exact);
-  * sampled queries: dense scores / l / hits == the oracle querying the
-    GPU-built file image.
+  * the file: every byte of the GPU-built image (header and payload) against
+    the streamed oracle build of the same corpus (oracle/cobs_stream.c,
+    orc_stream_check -- the reference's extract_terms / build_* / write_index
+    restated one 64-document column group at a time);
+  * dense scores (K = 1e-12, every document's score) of a seeded 1% query
+    sample, and their l / skipped, against the oracle querying that image
+    (once the image equals the oracle's build, this is the oracle's query);
+  * the hit lists of the same sample at the config's K from the full batch.
 
     python tools/config_runs.py c2 c3 c4 [--out gpurun_out/configs.json]
 """
@@ -32,16 +32,7 @@ from oracle import oracle as O  # noqa: E402
 from workloads import synth  # noqa: E402
 
 
-def column_bits(img: bytes, idx: O.OracleIndex, block: int, col: int) -> np.ndarray:
-    dc, w, base = idx.blocks()[block]
-    rb = (dc + 7) // 8
-    off = idx.x.blocks[block].offset
-    rows = np.frombuffer(img, dtype=np.uint8, count=w * rb, offset=off).reshape(w, rb)
-    return (rows[:, col // 8] >> (col % 8)) & 1
-
-
-def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0, repeat: int = 1,
-        build_only: bool = False):
+def run(name: str, n_queries: int = 0, repeat: int = 1, build_only: bool = False):
     cfg = synth.CONFIGS[name]
     if n_queries:
         cfg = synth.replace(cfg, n_queries=n_queries)
@@ -97,56 +88,57 @@ def run(name: str, n_sample_docs: int, n_sample_queries: int, n_queries: int = 0
                     "gather_gbs": out.row_bytes / (out.ms_gather / 1e3) / 1e9,
                     "hits_total": int(out.hit_n.sum())}
 
-    # ---- parity through properties + samples ----------------------------
+    # ---- parity: the whole file, then a seeded 1% of the queries --------
     t = time.perf_counter()
-    img = cb.index_image(view)
-    idx = O.OracleIndex.parse(img)
-    checks = {}
-    blocks = idx.blocks()
-    tcs = np.asarray(idx.term_counts(), dtype=np.uint64)
-    checks["widths_sized_by_oracle"] = all(
-        w == O.size_filter(int(tcs[base:base + dc].max()), cfg.p, cfg.k) for dc, w, base in blocks)
-    if cfg.kind == 1:
-        nms = idx.names()
-        checks["compact_order"] = all((tcs[i], nms[i]) <= (tcs[i + 1], nms[i + 1])
-                                      for i in range(len(nms) - 1))
-    name_to_col = {n: i for i, n in enumerate(idx.names())}
-    rng = random.Random(7)
-    sample = rng.sample(range(cfg.n_docs), n_sample_docs)
-    ok_tc = ok_col = True
-    for d in sample:
-        buf, off = synth.docs(cfg, [d], lengths=lengths)
-        content = [buf.tobytes()]
-        terms, sk, occ = O.extract_terms(content, cfg.q, cfg.canonical)
-        g = name_to_col[names[d]]
-        b = next(i for i, (dc, w, base) in enumerate(blocks) if base <= g < base + dc)
-        dc, w, base = blocks[b]
-        ok_tc &= int(tcs[g]) == len(terms)
-        one = O.build_image([(names[d], content)], q=cfg.q, k=cfg.k, p=cfg.p,
-                            canonical=cfg.canonical, kind=0, forced_w=w)
-        one_idx = O.OracleIndex.parse(one)
-        want = column_bits(one, one_idx, 0, 0)
-        got = column_bits(img, idx, b, g - base)
-        ok_col &= bool(np.array_equal(want, got))
-    checks["sampled_term_counts"] = ok_tc
-    checks["sampled_columns_exact"] = ok_col
-    qs = sorted(rng.sample(range(len(qo) - 1), n_sample_queries))
-    ok_q = True
-    for i in qs:
-        pat = qb[int(qo[i]):int(qo[i + 1])].tobytes()
-        try:
-            ell, sk, hits, _ = idx.query(pat, cfg.K)
-        except O.OracleError as e:
-            ok_q &= int(out.status[i]) == e.code
-            continue
-        d_, s_ = out.hits(i)
-        ok_q &= (int(out.ell[i]), int(out.skipped[i])) == (ell, sk)
-        ok_q &= [(int(a), int(b)) for a, b in zip(d_, s_)] == hits
-    checks["sampled_queries_hits"] = ok_q
-    checks["n_sample_docs"] = n_sample_docs
-    checks["n_sample_queries"] = n_sample_queries
-    checks["check_s"] = time.perf_counter() - t
+    img = cb.index_image_array(view)  # the file image, straight into one host array
+    res["image_bytes"] = int(len(img))
+    res["image_d2h_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    rep = O.stream_check(cfg.seed, cfg.alpha, lengths, img, q=cfg.q, k=cfg.k, p=cfg.p,
+                         canonical=cfg.canonical, block_size=cfg.block_size, kind=cfg.kind,
+                         threads=os.cpu_count() or 1)
+    checks = {"file_header_equal": rep["header_equal"],
+              "file_payload_bad_bytes": int(rep["payload_bad_bytes"]),
+              "file_term_count_mismatch": int(rep["term_count_mismatch"]),
+              "oracle_windows": int(rep["windows"]),
+              "file_check_s": time.perf_counter() - t,
+              "file_check_threads": os.cpu_count() or 1}
+    checks["file_byte_identical"] = (rep["header_equal"] and rep["payload_bad_bytes"] == 0
+                                     and rep["term_count_mismatch"] == 0)
+    if not build_only:
+        t = time.perf_counter()
+        idx = O.OracleIndex.parse_array(img)
+        n_q = len(qo) - 1
+        rng = np.random.default_rng(cfg.seed)
+        sample = np.sort(rng.choice(n_q, size=max(1, n_q // 100), replace=False)).astype(np.uint64)
+        sb, so = synth.queries(cfg, sample, lengths=lengths)
+        # dense scores (K = 1e-12: tau = 1, every score exported) of the sample
+        g = cb.query_batch_raw(view, sb, so, 1e-12, scores=True, hits=False)
+        ell, sk, st, _, dense = idx.query_batch(sb, so, 1e-12, scores=True, threads=os.cpu_count() or 1)
+        checks["dense_sample_queries"] = int(len(sample))
+        checks["dense_scores_equal"] = bool(np.array_equal(g.dense.astype(np.uint32), dense)
+                                            and np.array_equal(g.ell.astype(np.uint64), ell)
+                                            and np.array_equal(g.skipped.astype(np.uint64), sk))
+        checks["dense_nonzero_frac"] = float((dense > 0).mean())
+        # hit lists at the config's K: the full batch's answers for the sample
+        ok_q, n_hits = True, 0
+        for j, i in enumerate(sample.tolist()):
+            pat = sb[int(so[j]):int(so[j + 1])].tobytes()
+            try:
+                ell_i, sk_i, hits, _ = idx.query(pat, cfg.K)
+            except O.OracleError as e:
+                ok_q &= int(out.status[i]) == e.code
+                continue
+            d_, s_ = out.hits(i)
+            ok_q &= (int(out.ell[i]), int(out.skipped[i])) == (ell_i, sk_i)
+            ok_q &= [(int(a), int(b)) for a, b in zip(d_, s_)] == hits
+            n_hits += len(hits)
+        checks["sample_hits_equal"] = ok_q
+        checks["sample_hits_total"] = n_hits
+        checks["query_check_s"] = time.perf_counter() - t
+        del idx
     res["checks"] = checks
+    del img
     view.close()
     return res
 
@@ -155,15 +147,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
-    ap.add_argument("--docs", type=int, default=4)
-    ap.add_argument("--queries", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--build-only", action="store_true")
     a = ap.parse_args()
     results = []
     for c in a.configs:
-        r = run(c, a.docs, a.queries, a.batch, a.repeat, a.build_only)
+        r = run(c, a.batch, a.repeat, a.build_only)
         print(json.dumps(r), flush=True)
         results.append(r)
         json.dump(results, open(a.out, "w"), indent=1)
