@@ -13,14 +13,8 @@ struct DeviceIndex;
 
 constexpr int kFormatAuto = 0, kFormatFasta = 1, kFormatText = 2; // termizer.hpp:43-47
 
-struct FastaRecord {
-    std::string name, seq;
-};
-
-std::string read_file_bytes(const std::string& path);
-std::vector<FastaRecord> parse_fasta(const std::string& text);
-std::vector<FastaRecord> read_fasta_named(const std::string& path);
-std::vector<std::string> read_input(const std::string& path, int format);
+// Regular files named by `inputs` (directories expand to every regular file
+// below them, in path order): cli.cpp:60-82.
 std::vector<std::string> expand_inputs(const std::vector<std::string>& inputs);
 std::string doc_name_from_path(const std::string& path);
 

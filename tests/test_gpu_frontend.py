@@ -38,6 +38,38 @@ def write_tricky_fasta(path, docs_seqs, rng):
         f.write(b"\n".join(lines))
 
 
+def write_cr_edge_fasta(path, docs_seqs, rng):
+    """Line-ending corners of the reader (termizer.cpp:48-88): a '\r' inside
+    a line stays, one before '\n' goes, a final line without '\n' keeps its
+    '\r'; a line "\r>..." is sequence, not a header; "\r\n" alone is an empty
+    line; bytes >= 0x80 are not uppercased; chunk-crossing long lines."""
+    s1 = docs_seqs[0][:200]
+    body = (b"\r\n" + s1[:70] + b"\r\n" + b">h1\rmid  tail\r\n" + s1[10:110].lower() + b"\r" + s1[110:150]
+            + b"\n\r>" + s1[:80] + b"\n>h\xe9\xff x\n" + b"acgt\xe9" * 30 + b"\n>long\n"
+            + (s1 * 6000) + b"\n>" + b"\n" + rand(rng, 90) + b"\n>endcr\n" + s1[:64] + b"\r")
+    with open(path, "wb") as f:
+        f.write(body)
+
+
+@pytest.mark.gpu
+def test_query_fasta_line_ending_corners(gpu, tmp_path):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    import json
+    g = json.load(open(os.path.join(GDIR, "golden.json")))
+    rng = random.Random(9)
+    for name in ("compact_canon", "classic_k2"):
+        path = os.path.join(GDIR, name + ".cobs")
+        seqs = [s.encode() for d in g["files"][name]["docs"] for s in d[1]]
+        fa = str(tmp_path / (name + "_cr.fa"))
+        write_cr_edge_fasta(fa, seqs, rng)
+        view = cb.open_resident(path, gpu)
+        ref = O.RefIndex.open(path)
+        for K, top_t in [(0.5, 0), (1e-12, 2)]:
+            assert cb.query_fasta(view, fa, K, top_t) == ref.query_fasta_tsv(fa, K, top_t), (name, K, top_t)
+        view.close()
+
+
 @pytest.mark.gpu
 def test_query_fasta_tsv_matches_reference(gpu, tmp_path):
     if not O.ref_available():
@@ -74,6 +106,9 @@ def make_corpus_dir(root, rng):
         "b/nested/s4.txt": rand(rng, 500),                       # text: the whole file
         "b/nested/s5.txt": rand(rng, 100) + b"\n" + rand(rng, 100),
         "c_short.fa": b">tiny\nACGTACGT\n",                     # zero terms
+        "b/s6.fa": b"\r\n" + rand(rng, 40) + b"\r" + rand(rng, 60).lower() + b"\n\r>" + rand(rng, 70)
+                   + b"\n>y\n" + rand(rng, 80) + b"\r",                # line-ending corners
+        "b/s7.fa": b"",                                          # no records: a document with no strings
     }
     for rel, data in files.items():
         with open(os.path.join(root, rel), "wb") as f:
