@@ -18,6 +18,7 @@
 // A host batch too large for the free HBM runs as sub-batches (results
 // concatenated, one dense score width).
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -567,6 +568,19 @@ GatherFn pick_gather(int nt_needed, int kt, bool ef) {
 
 namespace {
 
+// More hits than one ordering pass may hold: kernel 3's sorts take an int
+// item count, and every hit needs ~12 bytes in the gather's pool plus ~40 in
+// the sort buffers.  query_batch re-runs such a batch as two halves.
+struct HitsOverflow {
+    uint64_t hits;
+};
+uint64_t hit_limit() {
+    if (const char* e = std::getenv("COBS_HIT_LIMIT")) return std::strtoull(e, nullptr, 10); // tests
+    size_t free_b = 0, total_b = 0;
+    COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    return std::min<uint64_t>(0x7fffffffull, free_b / 64);
+}
+
 // One batch through kernels 1-3; the caller holds ix.mu.  min_nt: at least
 // this many count bits (dense score width agreed over sub-batches).
 void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offsets, uint64_t n,
@@ -813,6 +827,7 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         COBS_CUDA(cudaEventRecord(ev[2], st));
         COBS_CUDA(cudaMemcpyAsync(&h_total, ws.hit_total.ptr, 8, cudaMemcpyDeviceToHost, st));
         COBS_CUDA(cudaStreamSynchronize(st));
+        if (want_hits && h_total > hit_limit()) throw HitsOverflow{h_total}; // caller splits the batch
         if (h_total <= ws.hit_cap) break;
         ws.hit_cap = h_total + h_total / 8;
         ws.hit_q.reserve(4 * ws.hit_cap);
@@ -953,7 +968,12 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     std::lock_guard<std::mutex> lock(ix.mu);
     COBS_CUDA(cudaSetDevice(ix.device));
     if ((flags & (COBS_Q_DEVICE_INPUT | COBS_Q_KEEP_DEVICE)) || n <= 1) {
-        query_batch_one(ix, patterns, offsets, n, K, top_t, flags, 1, R);
+        try {
+            query_batch_one(ix, patterns, offsets, n, K, top_t, flags, 1, R);
+        } catch (const HitsOverflow& h) {
+            throw UsageError("query: " + std::to_string(h.hits) +
+                             " hits exceed one ordering pass; submit the batch in parts");
+        }
         return;
     }
     const uint32_t q = ix.meta.params.q, k = ix.meta.params.k;
@@ -972,22 +992,35 @@ void query_batch(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* offse
     COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     uint64_t budget = std::max<uint64_t>(free_b / 2, 64ull << 20);
     if (const char* e = std::getenv("COBS_QUERY_BUDGET")) budget = std::strtoull(e, nullptr, 10);
-    if (total <= budget) {
-        query_batch_one(ix, patterns, offsets, n, K, top_t, flags, 1, R);
-        return;
-    }
     const int nt = bits_for(wmax);
     R = QueryResults();
     std::vector<uint64_t> sub_off;
-    for (uint64_t a = 0; a < n;) {
-        uint64_t b = a, c = 0;
-        while (b < n && (b == a || c + cost[b] <= budget)) c += cost[b++];
+    // queries [a, b) as one sub-batch; halved while their hits overflow
+    std::function<void(uint64_t, uint64_t)> run = [&](uint64_t a, uint64_t b) {
         sub_off.assign(offsets + a, offsets + b + 1);
         const uint64_t base = sub_off[0];
         for (uint64_t& o : sub_off) o -= base;
         QueryResults S;
-        query_batch_one(ix, patterns + base, sub_off.data(), b - a, K, top_t, flags, nt, S);
+        try {
+            query_batch_one(ix, patterns + base, sub_off.data(), b - a, K, top_t, flags, nt, S);
+        } catch (const HitsOverflow& h) {
+            if (b - a == 1)
+                throw UsageError("query: " + std::to_string(h.hits) + " hits of one pattern exceed one ordering pass");
+            const uint64_t mid = a + (b - a) / 2;
+            run(a, mid);
+            run(mid, b);
+            return;
+        }
         append_results(R, std::move(S));
+    };
+    if (total <= budget) {
+        run(0, n);
+        return;
+    }
+    for (uint64_t a = 0; a < n;) {
+        uint64_t b = a, c = 0;
+        while (b < n && (b == a || c + cost[b] <= budget)) c += cost[b++];
+        run(a, b);
         a = b;
     }
 }

@@ -160,3 +160,30 @@ def test_q32_raw_poly_t_and_high_codes(gpu, partition):
             check(img, pats, Ks=(1e-12, 0.5, 1.0), tops=(0, 3))
     finally:
         del os.environ["COBS_COUNT_PARTITION"]
+
+
+def test_hit_overflow_splits_batch(gpu):
+    """More hits than one ordering pass may hold (CUB's int item count, the
+    hit buffers): the batch is re-run in halves with identical answers
+    (COBS_HIT_LIMIT lowers the limit per call for the test); a single
+    pattern over the limit, or a device-input batch, is a usage error."""
+    import os
+    rng = random.Random(12)
+    docs = [(b"h%03d" % i, [rb(rng, 400, b"ACGT")]) for i in range(60)]
+    img = O.build_image(docs, k=1, block_size=16, kind=1)
+    pats = [docs[i][1][0][:200] for i in range(0, 60, 3)] + [rb(rng, 150, b"ACGT") for _ in range(7)]
+    view = cb.open_image(img, 0)
+    want = cb.query_batch(view, pats, 1e-12, 5)
+    os.environ["COBS_HIT_LIMIT"] = "100"   # each pattern hits ~every document
+    try:
+        got = cb.query_batch(view, pats, 1e-12, 5)
+        for i in range(len(pats)):
+            a, b = want.hits(i), got.hits(i)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert want.ell[i] == got.ell[i]
+        os.environ["COBS_HIT_LIMIT"] = "10"
+        with pytest.raises(ValueError, match="hits of one pattern exceed one ordering pass"):
+            cb.query_batch(view, pats[:2], 1e-12)
+    finally:
+        del os.environ["COBS_HIT_LIMIT"]
+    view.close()
