@@ -23,6 +23,7 @@
 //               the distinct ones.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -203,7 +204,8 @@ constexpr uint32_t kPcRunsPerThread = 16; // consecutive runs one thread rolls t
 constexpr uint32_t kPcRuns = 256 * kPcRunsPerThread; // runs (x kBRun windows) per chunk
 constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in shared memory
 constexpr uint32_t kPcMaxSlots = 16384; // largest dedup set (128 KB of shared memory)
-constexpr uint64_t kPcTarget = 2048;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
+constexpr uint64_t kPcTarget = 4096;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
+                                        // (A/B with 1x-mean sets: 1,024 / 2,048 / 4,096 -> C3 count 1.81 / 1.65 / 1.61 s)
 
 struct PcDoc {
     uint64_t run_lo, run_hi; // global run range of the document
@@ -563,7 +565,8 @@ __global__ void pc_bdoc_kernel(const PcDoc* docs, uint32_t ndocs, uint32_t* buck
 
 // one CTA per bucket: distinct keys through a shared-memory set sized to the
 // bucket; the count goes to the bucket's document
-__global__ void __launch_bounds__(256) pc_dedup_kernel(const uint32_t* off, uint64_t nbuckets,
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) pc_dedup_kernel(const uint32_t* off, uint64_t nbuckets,
                                                        const unsigned long long* keys, const uint32_t* bucket_doc,
                                                        unsigned long long* term_count, unsigned int* overflow,
                                                        uint32_t slots) {
@@ -577,34 +580,36 @@ __global__ void __launch_bounds__(256) pc_dedup_kernel(const uint32_t* off, uint
             ++S_log2;
         }
         __syncthreads(); // the previous bucket's inserts are done
-        for (uint32_t j = threadIdx.x; j < S; j += blockDim.x) s_tab[j] = 0ull;
+        for (uint32_t j = threadIdx.x; j < S / 2; j += blockDim.x)
+            reinterpret_cast<ulonglong2*>(s_tab)[j] = make_ulonglong2(0ull, 0ull);
         __syncthreads();
         uint32_t mine = 0;
         bool stuck = false;
         // Bucketised set: S/4 groups of 4 slots (32 bytes, two LDS.128); a key
-        // is looked up in its group with straight-line compares and claims the
-        // group's first empty slot, so most keys finish in one round.  Keys of
-        // a bucket are codes spread by the bucket's mix, so a 32-bit
-        // multiplicative hash suffices for the group.
-        const uint32_t G = S / 4;
+        // looks in its group and claims the group's first empty slot with one
+        // CAS (re-read on a lost race), or moves to the next group when all
+        // four hold other keys.  Keys of a bucket are codes spread by the
+        // bucket's mix, so a 32-bit multiplicative hash suffices for the group.
+        const uint32_t gmask = S / 4 - 1;
         auto insert = [&](unsigned long long key) {
             uint32_t g = ((static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * 0x9E3779B1u) >> (34 - S_log2);
-            for (uint32_t probes = 0; probes < G; ++probes, g = (g + 1) & (G - 1)) {
+            for (uint32_t probes = 0; probes <= gmask;) {
                 unsigned long long* grp = s_tab + 4 * g;
                 const ulonglong2 lo = *reinterpret_cast<const ulonglong2*>(grp);
                 const ulonglong2 hi = *reinterpret_cast<const ulonglong2*>(grp + 2);
                 if (lo.x == key || lo.y == key || hi.x == key || hi.y == key) return;
-                unsigned long long v[4] = {lo.x, lo.y, hi.x, hi.y};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (v[e] != 0ull) continue;
-                    const unsigned long long cur = atomicCAS(grp + e, 0ull, key);
-                    if (cur == 0ull) {
-                        ++mine;
-                        return;
-                    }
-                    if (cur == key) return;
+                const int e = lo.x == 0ull ? 0 : lo.y == 0ull ? 1 : hi.x == 0ull ? 2 : hi.y == 0ull ? 3 : 4;
+                if (e == 4) { // all four hold other keys
+                    g = (g + 1) & gmask;
+                    ++probes;
+                    continue;
                 }
+                const unsigned long long cur = atomicCAS(grp + e, 0ull, key);
+                if (cur == 0ull) {
+                    ++mine;
+                    return;
+                }
+                if (cur == key) return; // (else another key took the slot: look again)
             }
             stuck = true; // every group full: the wave is recounted
         };
@@ -948,7 +953,14 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             uint64_t kmax = std::min<uint64_t>((free_b / 2) / (two_level ? 16 : 8), 0xffffffffull);
             if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
-            const uint64_t max_buckets = kmax / (kPcTarget / 2) + 2 * n_docs + 1;
+            uint64_t target = kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
+            if (const char* e = std::getenv("COBS_PC_TARGET")) target = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
+            const uint64_t max_buckets = kmax / (target / 2) + 2 * n_docs + 1;
+            // slots >= slot_mul x mean bucket keys + slack: 1x (A/B knob
+            // COBS_PC_SLOT_MUL) -- the smaller sets let more CTAs share an SM
+            // (the dedup is bound by the shared-memory pipe), C3 count 1.81 -> 1.66 s
+            double slot_mul = 1.0;
+            if (const char* e = std::getenv("COBS_PC_SLOT_MUL")) slot_mul = std::atof(e);
             // plan every wave up front (documents in order, keys <= kmax); the
             // waves then run back to back without a host round trip
             struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup; };
@@ -961,11 +973,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 while (d1 < n_docs) {
                     const uint64_t W = doc_w[d1];
                     uint64_t nbk = 1;
-                    while (nbk * kPcTarget < W && nbk < kPcHist) nbk <<= 1;
+                    while (nbk * target < W && nbk < kPcHist) nbk <<= 1;
                     // the set must hold a bucket's distinct keys: mean W / nbk, plus slack
                     const uint64_t mean = (W + nbk - 1) / nbk;
                     uint64_t slots = 256;
-                    while (slots < 2 * mean + 8 * 64 && slots < kPcMaxSlots) slots <<= 1;
+                    while (slots < slot_mul * mean + 8 * 64 && slots < kPcMaxSlots) slots <<= 1;
                     if (d1 > d0 && (wv.keys + W > kmax || wv.nbuck + nbk > max_buckets)) break;
                     wv.slots = std::max(wv.slots, slots);
                     PcDoc D{};
@@ -1027,7 +1039,12 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             auto hist = sym_bits ? pc_hist_kernel<0, kSymBits> : q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
             auto scat = q == 31 ? pc_scatter_kernel<31> : pc_scatter_kernel<0>;
             COBS_CUDA(cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
-            COBS_CUDA(cudaFuncSetAttribute(pc_dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
+            // dedup CTA size (A/B knob COBS_PC_DEDUP_THREADS = 256 / 512 / 1024)
+            int dthreads = 256;
+            if (const char* e = std::getenv("COBS_PC_DEDUP_THREADS")) dthreads = std::atoi(e);
+            auto dedup = dthreads >= 1024 ? pc_dedup_kernel<1024> : dthreads >= 512 ? pc_dedup_kernel<512> : pc_dedup_kernel<256>;
+            dthreads = dthreads >= 1024 ? 1024 : dthreads >= 512 ? 512 : 256;
+            COBS_CUDA(cudaFuncSetAttribute(dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
                 const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
@@ -1068,7 +1085,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 }
                 if (wv.nchunk) {
                     if (!two_level) scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
-                    pc_dedup_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), 256, wv.slots * 8, st>>>(
+                    dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dthreads, wv.slots * 8, st>>>(
                         d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
                         d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
                         static_cast<uint32_t>(wv.slots));
@@ -1145,6 +1162,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         float ms_count = 0;
         cudaEventElapsedTime(&ms_count, e0, e1);
         g_timing.ms_count = ms_count;
+        if (std::getenv("COBS_BUILD_DEBUG"))
+            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u\n",
+                         ms_count, use_pc ? 1 : 0, g_timing.count_waves, g_timing.count_fallback_waves, fill_rpt);
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
     }
 
