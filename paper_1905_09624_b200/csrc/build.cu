@@ -23,6 +23,7 @@
 //               the distinct ones.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -977,7 +978,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     // the set must hold a bucket's distinct keys: mean W / nbk, plus slack
                     const uint64_t mean = (W + nbk - 1) / nbk;
                     uint64_t slots = 256;
-                    while (slots < slot_mul * mean + 8 * 64 && slots < kPcMaxSlots) slots <<= 1;
+                    // (+ 6 sigma of a bucket's key count + slack: the fullest
+                    // bucket stays below ~90 % load)
+                    while (slots < slot_mul * 1.15 * mean + 6.0 * std::sqrt(static_cast<double>(mean)) + 256 &&
+                           slots < kPcMaxSlots)
+                        slots <<= 1;
                     if (d1 > d0 && (wv.keys + W > kmax || wv.nbuck + nbk > max_buckets)) break;
                     wv.slots = std::max(wv.slots, slots);
                     PcDoc D{};
