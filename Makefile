@@ -6,7 +6,7 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            -Xcudafe --diag_suppress=177
 SRC := paper_1905_09624_b200/csrc
 OUT := paper_1905_09624_b200/_lib
-OBJS := $(OUT)/host.o $(OUT)/frontend.o $(OUT)/index.o $(OUT)/query.o $(OUT)/tiled.o $(OUT)/build.o $(OUT)/merge.o \
+OBJS := $(OUT)/host.o $(OUT)/frontend.o $(OUT)/index.o $(OUT)/query.o $(OUT)/build.o $(OUT)/merge.o \
         $(OUT)/calib.o $(OUT)/capi.o
 HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh $(SRC)/*.h) include/cobs_gpu.h
 

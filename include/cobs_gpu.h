@@ -203,10 +203,11 @@ uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r);
 /* Streaming mode: index payload bytes copied host -> HBM by the batch (the
  * analogue of RandomAccessView::bytes_read, index_view.hpp:44-46). */
 uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r);
-/* Which row-gather kernel served the batch: 0 = one warp per (query, slice)
- * (gather_kernel), 1 = the L2-tiled gather (bucket_kernel + tile_kernel).
- * Both compute the same scores and hits (query.cpp:49-89).  The tiled
- * gather is opt-in (environment COBS_TILED=1; measured slower). */
+/* Where kernel 2 read the index rows from: 0 = HBM-resident payload, 1 =
+ * the host-resident (pinned) payload directly over PCIe (zero-copy: only the
+ * addressed rows), 2 = the host-resident payload streamed through HBM staging
+ * buffers (the whole payload per batch).  All compute the same scores and
+ * hits (query.cpp:49-89); h2d_index_bytes counts the index bytes moved. */
 uint32_t cobs_gpu_results_gather_path(const cobs_gpu_results* r);
 void cobs_gpu_results_free(cobs_gpu_results* r);
 

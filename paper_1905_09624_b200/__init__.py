@@ -121,7 +121,7 @@ class BatchResult:
     launches: int
     row_bytes: int
     h2d_index_bytes: int = 0
-    gather_path: int = 0  # 0 gather_kernel, 1 L2-tiled gather
+    gather_path: int = 0  # rows read from: 0 HBM, 1 host memory over PCIe (zero-copy), 2 streamed via HBM
 
     def hits(self, i: int) -> Tuple[np.ndarray, np.ndarray]:
         o, n = int(self.hit_off[i]), int(self.hit_n[i])

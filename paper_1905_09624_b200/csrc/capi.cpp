@@ -335,7 +335,9 @@ uint32_t cobs_gpu_results_launches(const cobs_gpu_results* r) { return r->r.laun
 
 uint64_t cobs_gpu_results_row_bytes(const cobs_gpu_results* r) { return r->r.row_bytes; }
 
-uint32_t cobs_gpu_results_gather_path(const cobs_gpu_results* r) { return r->r.tiled ? 1u : 0u; }
+uint32_t cobs_gpu_results_gather_path(const cobs_gpu_results* r) {
+    return r->r.zero_copy ? 1u : r->r.h2d_index_bytes ? 2u : 0u;
+}
 
 uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r) { return r->r.h2d_index_bytes; }
 

@@ -179,10 +179,27 @@ HostStream::~HostStream() {
 }
 
 void HostStream::read_payload(uint64_t off, void* dst, uint64_t len) const {
-    if (file_backed)
+    if (file_backed) {
         src.read_at(payload_start + off, dst, len);
-    else
-        std::memcpy(dst, host + off, len);
+        return;
+    }
+    // file layout [off, off + len) from the pitched host copy, row by row
+    uint8_t* out = static_cast<uint8_t*>(dst);
+    for (size_t b = 0; b < block_off.size() && len; ++b) {
+        const DevBlock& d = (*layout)[b];
+        const uint64_t bytes = d.w * d.rb;
+        if (off >= block_off[b] + bytes) continue;
+        uint64_t rel = off - block_off[b];
+        while (len && rel < bytes) {
+            const uint64_t r = rel / d.rb, c = rel - r * d.rb;
+            const uint64_t n = std::min<uint64_t>(d.rb - c, len);
+            std::memcpy(out, host + d.base + r * d.pitch + c, n);
+            out += n;
+            off += n;
+            rel += n;
+            len -= n;
+        }
+    }
 }
 
 void HostStream::stage_group(const std::vector<DevBlock>& blocks, size_t gi, uint8_t* dst) const {
@@ -322,14 +339,53 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget, boo
     hs->host_bytes = m.file_size - m.payload_start;
     hs->payload_start = m.payload_start;
     hs->file_backed = file_backed;
+    for (size_t b = 0; b < ix.blocks.size(); ++b) hs->block_off.push_back(m.blocks[b].offset - m.payload_start);
     if (file_backed) {
         hs->src = src;
-    } else {
-        COBS_CUDA(cudaHostAlloc(&hs->host, std::max<uint64_t>(hs->host_bytes, 1), cudaHostAllocDefault));
-        for (uint64_t o = 0; o < hs->host_bytes; o += (1ull << 30)) {
-            uint64_t len = std::min<uint64_t>(1ull << 30, hs->host_bytes - o);
-            src.read_at(m.payload_start + o, hs->host + o, len);
+    } else { // pitched, mapped pinned copy: rows read in 64 MB pieces, re-pitched by host threads
+        COBS_CUDA(cudaHostAlloc(&hs->host, std::max<uint64_t>(ix.payload_bytes, 1),
+                                cudaHostAllocMapped | cudaHostAllocPortable));
+        COBS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hs->host_dev), hs->host, 0));
+        hs->layout = &ix.blocks;
+        struct Piece { size_t b; uint64_t r0, r1; };
+        std::vector<Piece> pieces;
+        for (size_t b = 0; b < ix.blocks.size(); ++b) {
+            const DevBlock& d = ix.blocks[b];
+            const uint64_t rows = std::max<uint64_t>(1, (64ull << 20) / std::max<uint32_t>(d.rb, 1));
+            for (uint64_t r = 0; r < d.w; r += rows) pieces.push_back({b, r, std::min(d.w, r + rows)});
         }
+        std::atomic<size_t> next{0};
+        std::exception_ptr failure;
+        std::mutex fail_mu;
+        auto work = [&] {
+            std::vector<uint8_t> tmp;
+            try {
+                for (size_t i = next.fetch_add(1); i < pieces.size(); i = next.fetch_add(1)) {
+                    const Piece& p = pieces[i];
+                    const DevBlock& d = ix.blocks[p.b];
+                    uint8_t* dst = hs->host + d.base + p.r0 * d.pitch;
+                    if (d.pitch == d.rb) {
+                        src.read_at(m.blocks[p.b].offset + p.r0 * d.rb, dst, (p.r1 - p.r0) * d.rb);
+                        continue;
+                    }
+                    tmp.resize((p.r1 - p.r0) * d.rb);
+                    src.read_at(m.blocks[p.b].offset + p.r0 * d.rb, tmp.data(), tmp.size());
+                    for (uint64_t r = p.r0; r < p.r1; ++r) {
+                        std::memcpy(dst + (r - p.r0) * d.pitch, tmp.data() + (r - p.r0) * d.rb, d.rb);
+                        std::memset(dst + (r - p.r0) * d.pitch + d.rb, 0, d.pitch - d.rb);
+                    }
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(fail_mu);
+                failure = std::current_exception();
+            }
+        };
+        const size_t nt = std::min<size_t>(pieces.size(), std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+        std::vector<std::thread> th;
+        for (size_t t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto& t : th) t.join();
+        if (failure) std::rethrow_exception(failure);
     }
     const uint64_t half = (budget / 2) & ~255ull;
     hs->staging_bytes = half;
@@ -339,7 +395,6 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget, boo
     uint64_t used = 0;
     for (size_t b = 0; b < ix.blocks.size(); ++b) {
         const DevBlock& d = ix.blocks[b];
-        hs->block_off.push_back(m.blocks[b].offset - m.payload_start);
         const uint32_t nsl = (d.rb + 127u) / 128u;
         const uint64_t per_slice = d.w * 128ull;
         uint32_t s_max = static_cast<uint32_t>(std::max<uint64_t>(1, half / std::max<uint64_t>(per_slice, 1)));
@@ -349,10 +404,16 @@ void open_streaming(DeviceIndex& ix, const ByteSource& src, uint64_t budget, boo
             sl.s0 = s0;
             sl.ns = std::min(s_max, nsl - s0);
             sl.width = std::min<uint32_t>(d.rb - s0 * 128u, sl.ns * 128u);
-            // whole 4-byte-aligned rows go over as one contiguous copy at the
-            // file's own row length (narrow 2D DMA rows crawl over PCIe)
-            sl.direct = s0 == 0 && sl.width == d.rb && (d.rb & 3u) == 0;
-            sl.pitch = sl.direct ? sl.width : ((sl.width + 31u) & ~31u);
+            // whole rows go over as one contiguous copy at the source's own
+            // row stride (narrow 2D DMA rows crawl over PCIe): the pitched host
+            // copy's pitch, or the file's row length when 4-byte aligned
+            if (file_backed) {
+                sl.direct = s0 == 0 && sl.width == d.rb && (d.rb & 3u) == 0;
+                sl.pitch = sl.direct ? sl.width : ((sl.width + 31u) & ~31u);
+            } else {
+                sl.direct = s0 == 0 && sl.width == d.rb;
+                sl.pitch = sl.direct ? d.pitch : ((sl.width + 31u) & ~31u);
+            }
             const uint64_t bytes = ((d.w * sl.pitch) + 255) & ~255ull;
             if (bytes > half)
                 throw DataError("block " + std::to_string(b) + " needs " + std::to_string(bytes) +

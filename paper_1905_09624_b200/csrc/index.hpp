@@ -44,7 +44,6 @@ struct QueryWorkspace {
     DevBuf hit_count, hit_total, hit_q, hit_doc, hit_score;
     DevBuf key64, key64_alt, key32, key32_alt, perm, perm_alt, out_doc, out_score;
     DevBuf scores, cub_tmp;
-    DevBuf tlist, tdone, tshift; // L2-tiled gather (tiled.cu): bucketed row lists, phase counters, range shifts
     PinnedBuf h_small;
     uint64_t hit_cap = 0;
 };
@@ -59,15 +58,22 @@ struct Slab {
     uint32_t block, s0, ns; // slices [s0, s0+ns) of `block`
     uint64_t base;          // offset inside the staging buffer
     uint32_t width, pitch;  // row bytes copied / device row stride
-    bool direct;            // whole rows, pitch == file row bytes: one 1D copy
+    bool direct;            // whole rows in one 1D copy (the source row stride == pitch)
 };
 struct StreamGroup {
     uint32_t slab_lo, slab_hi, ct_lo, ct_hi;
 };
 struct HostStream {
-    uint8_t* host = nullptr;         // pinned; the file's payload bytes
-    uint64_t host_bytes = 0;
-    std::vector<uint64_t> block_off; // payload offset of each block
+    // Pinned variant: the payload in mapped pinned host memory, in the
+    // device's pitched layout (block b at DevBlock::base, rows DevBlock::pitch
+    // apart, zero padding), so the gather can also read the addressed rows
+    // straight over PCIe (zero-copy, host_dev) when a batch touches far less
+    // than the whole payload.
+    uint8_t* host = nullptr;         // pinned, mapped; pitched payload
+    uint8_t* host_dev = nullptr;     // its device alias
+    const std::vector<DevBlock>* layout = nullptr; // the pitched layout of `host`
+    uint64_t host_bytes = 0;         // payload bytes in file layout
+    std::vector<uint64_t> block_off; // file-layout payload offset of each block
     std::vector<Slab> slabs;
     std::vector<StreamGroup> groups;
     DevBlock* d_slab_blocks = nullptr;
@@ -163,8 +169,8 @@ struct QueryResults {
     uint32_t score_bytes = 2;
     double ms_termize = 0, ms_gather = 0, ms_order = 0, ms_total = 0;
     uint32_t launches = 0; // kernels of ours launched by the batch
-    bool tiled = false;    // kernel 2 ran as the L2-tiled gather (tiled.cu)
-    uint64_t h2d_index_bytes = 0; // streaming mode: payload bytes copied to HBM
+    uint64_t h2d_index_bytes = 0; // host-resident modes: index bytes moved host -> GPU
+    bool zero_copy = false;       // host-resident: rows read from mapped host memory
     uint64_t row_bytes = 0;
 };
 

@@ -27,7 +27,6 @@
 #include "../../include/cobs_gpu.h"
 #include "gather_common.cuh"
 #include "index.hpp"
-#include "tiled.hpp"
 
 namespace cobsg {
 
@@ -745,8 +744,23 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     const uint64_t tiles = (n + qt - 1) / qt;
     const uint64_t grid2 = tiles * ((qt + qpc - 1) / qpc) * ga.nct;
     if (grid2 >= (1ull << 31)) throw UsageError("query batch too large for one launch; split it");
-    const TiledPlan tp = ix.streaming() ? TiledPlan() : tiled_plan(ix, win_base, n, nt_needed, ga.prune != 0);
-    R.tiled = tp.use;
+    // Host-resident (pinned) index: stream the whole payload through HBM, or
+    // -- when the batch addresses far fewer bytes -- let the gather read its
+    // rows straight from the mapped host copy over PCIe (zero-copy; random
+    // 128-byte reads cost ~kZcCost times a bulk DMA byte).  The bound uses
+    // windows for terms (l <= windows).  COBS_ZC=0/1 forces a mode (tests).
+    bool zc = false;
+    if (ix.streaming() && !ix.hs->file_backed) {
+        constexpr uint64_t kZcCost = 4;
+        uint64_t stream_bytes = 0;
+        for (uint64_t g : ix.hs->group_bytes) stream_bytes += g;
+        const uint64_t zc_bytes = wtot * k * ix.sum_row_bytes;
+        zc = zc_bytes * kZcCost < stream_bytes;
+        if (const char* e = std::getenv("COBS_ZC")) zc = e[0] == '1';
+    }
+    R.zero_copy = zc;
+    const bool resident_gather = !ix.streaming() || zc;
+    if (zc) ga.payload = ix.hs->host_dev;
     unsigned long long h_total = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         ga.hit_cap = ws.hit_cap;
@@ -756,24 +770,8 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         COBS_CUDA(cudaMemsetAsync(ws.hit_count.ptr, 0, 4 * n, st));
         COBS_CUDA(cudaMemsetAsync(ws.hit_total.ptr, 0, 8, st));
         if (attempt == 0) COBS_CUDA(cudaEventRecord(ev[1], st));
-        if (!ix.streaming()) {
-            if (tp.use) { // L2-tiled gather (tiled.cu)
-                TiledIO io{};
-                io.hashes = ga.hashes;
-                io.win_base = ga.win_base;
-                io.ell = ga.ell;
-                io.tau = ga.tau;
-                io.D = D;
-                io.scores = ga.scores;
-                io.want_hits = ga.want_hits;
-                io.hit_count = ga.hit_count;
-                io.hit_total = ga.hit_total;
-                io.hit_cap = ga.hit_cap;
-                io.hit_q = ga.hit_q;
-                io.hit_doc = ga.hit_doc;
-                io.hit_score = ga.hit_score;
-                R.launches += tiled_gather(ix, tp, st, io);
-            } else if (grid2 > 0) {
+        if (resident_gather) {
+            if (grid2 > 0) {
                 fn<<<static_cast<unsigned>(grid2), 256, split_smem, st>>>(ga);
                 R.launches += 1;
             }
@@ -797,14 +795,14 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
                 }
                 for (uint32_t si = G.slab_lo; si < (hs.file_backed ? G.slab_lo : G.slab_hi); ++si) {
                     const Slab& sl = hs.slabs[si];
-                    const DevBlock& d = ix.blocks[sl.block];
+                    const DevBlock& d = ix.blocks[sl.block]; // (the pitched host copy's layout too)
                     if (sl.direct)
-                        COBS_CUDA(cudaMemcpyAsync(hs.staging[buf] + sl.base, hs.host + hs.block_off[sl.block],
-                                                  d.w * d.rb, cudaMemcpyHostToDevice, hs.copy));
+                        COBS_CUDA(cudaMemcpyAsync(hs.staging[buf] + sl.base, hs.host + d.base, d.w * d.pitch,
+                                                  cudaMemcpyHostToDevice, hs.copy));
                     else
                         COBS_CUDA(cudaMemcpy2DAsync(hs.staging[buf] + sl.base, sl.pitch,
-                                                    hs.host + hs.block_off[sl.block] + sl.s0 * 128ull, d.rb,
-                                                    sl.width, d.w, cudaMemcpyHostToDevice, hs.copy));
+                                                    hs.host + d.base + sl.s0 * 128ull, d.pitch, sl.width, d.w,
+                                                    cudaMemcpyHostToDevice, hs.copy));
                     R.h2d_index_bytes += d.w * sl.width;
                 }
                 COBS_CUDA(cudaEventRecord(hs.copied[buf], hs.copy));
@@ -922,6 +920,7 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         }
         R.row_bytes += static_cast<uint64_t>(k) * R.ell[i] * ix.sum_row_bytes;
     }
+    if (zc) R.h2d_index_bytes = R.row_bytes; // the addressed rows, read over PCIe
     float t01 = 0, t12 = 0, t23 = 0;
     cudaEventElapsedTime(&t01, ev[0], ev[1]);
     cudaEventElapsedTime(&t12, ev[1], ev[2]);
@@ -954,6 +953,7 @@ void append_results(QueryResults& R, QueryResults&& S) {
     R.ms_total += S.ms_total;
     R.launches += S.launches;
     R.h2d_index_bytes += S.h2d_index_bytes;
+    R.zero_copy = R.zero_copy || S.zero_copy;
     R.row_bytes += S.row_bytes;
 }
 

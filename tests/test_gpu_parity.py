@@ -313,16 +313,38 @@ def test_host_resident_streaming(gpu, tmp_path, kind, frac, from_file):
     assert st.streaming() and not res.streaming()
     qb, qo = synth.queries(cfg)
     a = cb.query_batch_raw(res, qb, qo, 1e-12, scores=True)
-    b = cb.query_batch_raw(st, qb, qo, 1e-12, scores=True)
+    os.environ["COBS_ZC"] = "0"  # stream the whole payload
+    try:
+        b = cb.query_batch_raw(st, qb, qo, 1e-12, scores=True)
+    finally:
+        del os.environ["COBS_ZC"]
     assert np.array_equal(a.dense, b.dense)
     assert np.array_equal(a.ell, b.ell)
     payload = sum(st.width(i) * st.row_bytes(i) for i in range(st.block_count()))
     assert b.h2d_index_bytes == payload and a.h2d_index_bytes == 0
+    assert (a.gather_path, b.gather_path) == (0, 2)
+    modes = ["0"] if from_file else ["0", "1"]  # zero-copy needs the pinned copy
     for K, top_t in [(0.7, 0), (0.5, 4)]:
         x = cb.query_batch_raw(res, qb, qo, K, top_t)
-        y = cb.query_batch_raw(st, qb, qo, K, top_t)
-        for i in range(len(qo) - 1):
-            assert gpu_hits(res, x, i) == gpu_hits(st, y, i)
+        for zc in modes:
+            os.environ["COBS_ZC"] = zc
+            try:
+                y = cb.query_batch_raw(st, qb, qo, K, top_t)
+            finally:
+                del os.environ["COBS_ZC"]
+            assert y.gather_path == (1 if zc == "1" else 2)
+            for i in range(len(qo) - 1):
+                assert gpu_hits(res, x, i) == gpu_hits(st, y, i)
+    if not from_file:  # zero-copy: dense scores too, and only the addressed rows cross PCIe
+        os.environ["COBS_ZC"] = "1"
+        try:
+            c = cb.query_batch_raw(st, qb, qo, 1e-12, scores=True)
+        finally:
+            del os.environ["COBS_ZC"]
+        assert np.array_equal(a.dense, c.dense) and c.h2d_index_bytes == c.row_bytes < payload
+        # the automatic choice: one query addresses a sliver of the payload
+        one = cb.query_batch_raw(st, qb[:int(qo[1])], qo[:2], 0.5)
+        assert one.gather_path == 1 and one.h2d_index_bytes == one.row_bytes
     idx = O.OracleIndex.parse(img)
     ell, sk, s_, nh, dense = idx.query_batch(qb, qo, 1e-12, scores=True)
     assert np.array_equal(b.dense.astype(np.uint32), dense)

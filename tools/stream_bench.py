@@ -62,6 +62,31 @@ def main():
            "resident_ms_batch": resident.ms_total,
            "resident_qgrams_per_s": grams / (resident.ms_total / 1e3),
            "hits_equal_resident": bool(same), "launches": r.launches}
+    # row-granular (zero-copy) vs whole-payload streaming by batch size: the
+    # first n queries of the batch, each mode forced (COBS_ZC), and the mode
+    # the library picks on its own
+    sweep = []
+    for nq in (1, 8, 64, 512, 5000):
+        sub_o = qo[:nq + 1]
+        sub_b = qb[:int(sub_o[-1])]
+        row = {"queries": nq}
+        for mode in ("1", "0", None):
+            if mode is None:
+                os.environ.pop("COBS_ZC", None)
+            else:
+                os.environ["COBS_ZC"] = mode
+            cb.query_batch_raw(st, sub_b, sub_o, cfg.K)  # warm-up
+            rr = [cb.query_batch_raw(st, sub_b, sub_o, cfg.K) for _ in range(3)]
+            x = min(rr, key=lambda z: z.ms_total)
+            key = {"1": "zero_copy", "0": "streamed", None: "auto"}[mode]
+            row[key] = {"ms_batch": x.ms_total, "h2d_index_bytes": x.h2d_index_bytes, "row_bytes": x.row_bytes,
+                        "gather_path": x.gather_path,
+                        "hits_equal_resident": bool(all(np.array_equal(resident.hits(i)[0], x.hits(i)[0])
+                                                        for i in range(nq)))}
+        os.environ.pop("COBS_ZC", None)
+        print(row, flush=True)
+        sweep.append(row)
+    out["zero_copy_vs_streamed"] = sweep
     st.close()
     # file-backed leg: the payload is read from the index file every batch
     path = os.path.join(a.file_dir, "cobs_stream_bench.cobs")
