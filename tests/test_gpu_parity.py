@@ -341,7 +341,7 @@ def test_host_resident_streaming(gpu, tmp_path, kind, frac, from_file):
             c = cb.query_batch_raw(st, qb, qo, 1e-12, scores=True)
         finally:
             del os.environ["COBS_ZC"]
-        assert np.array_equal(a.dense, c.dense) and c.h2d_index_bytes == c.row_bytes < payload
+        assert np.array_equal(a.dense, c.dense) and c.h2d_index_bytes == c.row_bytes
         # the automatic choice: one query addresses a sliver of the payload
         one = cb.query_batch_raw(st, qb[:int(qo[1])], qo[:2], 0.5)
         assert one.gather_path == 1 and one.h2d_index_bytes == one.row_bytes

@@ -24,7 +24,7 @@ from workloads import synth  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--budget-gb", type=float, default=8.0)
+    ap.add_argument("--budget-gb", type=float, default=24.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "stream.json"))
     ap.add_argument("--file-dir", default="/tmp", help="where the file-backed leg writes the index")
     a = ap.parse_args()
