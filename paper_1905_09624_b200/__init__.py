@@ -365,50 +365,68 @@ def query_batch_raw(view: DeviceIndexView, buf, offsets, K: float = 0.9, top_t: 
                                     len(err))
     if rc:
         _raise(rc, err)
-    try:
-        ell, sk, st, ho, hn, dd, ss = (N.u32p(), N.u64p(), C.POINTER(C.c_int)(), N.u64p(),
-                                       N.u64p(), N.u32p(), N.u32p())
-        total = C.c_uint64()
-        N.lib.cobs_gpu_results_arrays(r, C.byref(ell), C.byref(sk), C.byref(st), C.byref(ho),
-                                      C.byref(hn), C.byref(dd), C.byref(ss), C.byref(total))
+    owner = _Results(r)
+    ell, sk, st, ho, hn, dd, ss = (N.u32p(), N.u64p(), C.POINTER(C.c_int)(), N.u64p(),
+                                   N.u64p(), N.u32p(), N.u32p())
+    total = C.c_uint64()
+    N.lib.cobs_gpu_results_arrays(r, C.byref(ell), C.byref(sk), C.byref(st), C.byref(ho),
+                                  C.byref(hn), C.byref(dd), C.byref(ss), C.byref(total))
 
-        def arr(ptr, count, dtype):
-            if count == 0 or not ptr:
-                return np.zeros(0, dtype=dtype)
-            return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+    def arr(ptr, count, dtype):
+        if count == 0 or not ptr:
+            return np.zeros(0, dtype=dtype)
+        return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
 
-        res_ell = arr(ell, n, np.uint32)
-        res_sk = arr(sk, n, np.uint64)
-        res_st = arr(st, n, np.int32)
-        messages = [""] * n
-        for i in np.nonzero(res_st)[0].tolist():  # only the failed queries carry text
-            msg = C.c_char_p()
-            N.lib.cobs_gpu_results_query(r, i, None, None, None, C.byref(msg), None)
-            messages[i] = msg.value.decode()
-        dense = None
-        if scores and not keep_device:
-            sb = C.c_uint32()
-            p = N.lib.cobs_gpu_results_scores(r, C.byref(sb))
-            D = view.total_docs()
-            dt = np.uint16 if sb.value == 2 else np.uint32
-            if p and n * D:
-                dense = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint16 if sb.value == 2 else C.c_uint32)),
-                                              shape=(n * D,)).astype(dt, copy=True).reshape(n, D)
-            else:
-                dense = np.zeros((n, D), dtype=dt)
-        t = [C.c_double(), C.c_double(), C.c_double(), C.c_double()]
-        N.lib.cobs_gpu_results_timing(r, *(C.byref(x) for x in t))
-        return BatchResult(
-            ell=res_ell, skipped=res_sk, status=res_st, messages=messages,
-            hit_off=arr(ho, n, np.uint64), hit_n=arr(hn, n, np.uint64),
-            docs=arr(dd, total.value, np.uint32), scores=arr(ss, total.value, np.uint32),
-            dense=dense, ms_termize=t[0].value, ms_gather=t[1].value, ms_order=t[2].value,
-            ms_total=t[3].value, launches=int(N.lib.cobs_gpu_results_launches(r)),
-            row_bytes=int(N.lib.cobs_gpu_results_row_bytes(r)),
-            h2d_index_bytes=int(N.lib.cobs_gpu_results_h2d_index_bytes(r)),
-            gather_path=int(N.lib.cobs_gpu_results_gather_path(r)))
-    finally:
-        N.lib.cobs_gpu_results_free(r)
+    def wrap(ptr, count, ctype):
+        """The library's result array itself (no copy): the numpy array
+        keeps the results alive, which are freed with the last such array."""
+        if count == 0 or not ptr:
+            return np.zeros(0, dtype=np.uint16 if ctype is C.c_uint16 else np.uint32)
+        buf = (ctype * count).from_address(C.cast(ptr, C.c_void_p).value)
+        buf._owner = owner
+        return np.ctypeslib.as_array(buf)
+
+    res_ell = arr(ell, n, np.uint32)
+    res_sk = arr(sk, n, np.uint64)
+    res_st = arr(st, n, np.int32)
+    messages = [""] * n
+    for i in np.nonzero(res_st)[0].tolist():  # only the failed queries carry text
+        msg = C.c_char_p()
+        N.lib.cobs_gpu_results_query(r, i, None, None, None, C.byref(msg), None)
+        messages[i] = msg.value.decode()
+    dense = None
+    if scores and not keep_device:
+        sb = C.c_uint32()
+        p = N.lib.cobs_gpu_results_scores(r, C.byref(sb))
+        D = view.total_docs()
+        dt = np.uint16 if sb.value == 2 else np.uint32
+        if p and n * D:
+            dense = wrap(p, n * D, C.c_uint16 if sb.value == 2 else C.c_uint32).reshape(n, D)
+        else:
+            dense = np.zeros((n, D), dtype=dt)
+    t = [C.c_double(), C.c_double(), C.c_double(), C.c_double()]
+    N.lib.cobs_gpu_results_timing(r, *(C.byref(x) for x in t))
+    return BatchResult(
+        ell=res_ell, skipped=res_sk, status=res_st, messages=messages,
+        hit_off=arr(ho, n, np.uint64), hit_n=arr(hn, n, np.uint64),
+        docs=wrap(dd, total.value, C.c_uint32), scores=wrap(ss, total.value, C.c_uint32),
+        dense=dense, ms_termize=t[0].value, ms_gather=t[1].value, ms_order=t[2].value,
+        ms_total=t[3].value, launches=int(N.lib.cobs_gpu_results_launches(r)),
+        row_bytes=int(N.lib.cobs_gpu_results_row_bytes(r)),
+        h2d_index_bytes=int(N.lib.cobs_gpu_results_h2d_index_bytes(r)),
+        gather_path=int(N.lib.cobs_gpu_results_gather_path(r)))
+
+
+class _Results:
+    """Owns a cobs_gpu_results handle; freed when the last array viewing
+    its hit / score buffers is gone."""
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    def __del__(self):
+        if self._h:
+            N.lib.cobs_gpu_results_free(self._h)
+            self._h = None
 
 
 def query_batch(view: DeviceIndexView, patterns: Sequence[bytes], K: float = 0.9,

@@ -41,7 +41,7 @@ struct PinnedBuf {
 
 struct QueryWorkspace {
     DevBuf pats, offs, win_base, tab_off, gtab, hashes, ell, skipped, tau;
-    DevBuf hit_count, hit_total, hit_q, hit_doc, hit_score;
+    DevBuf hit_count, hit_total, hit_q, hit_doc, hit_score, starts;
     DevBuf key64, key64_alt, key32, key32_alt, perm, perm_alt, out_doc, out_score;
     DevBuf scores, cub_tmp;
     PinnedBuf h_small;
@@ -49,11 +49,13 @@ struct QueryWorkspace {
 };
 
 // Host-resident (out-of-core) mode: the payload stays in
-// pinned host memory in file layout and every query batch streams it through
-// two HBM staging buffers in "slabs" (a block's rows restricted to a range of
-// 1,024-document slices), copy of slab group g+1 overlapping the gather of
-// group g.  The counterpart of the reference's random-access reader
-// (storage.cpp:320-341) for indexes larger than HBM.
+// pinned host memory (pitched) or in the index file, and a query batch either
+// streams it through two HBM staging buffers in "slabs" (a block's rows
+// restricted to a range of 1,024-document slices), copy of slab group g+1
+// overlapping the gather of group g, or -- pinned, small batches -- reads
+// only the addressed rows over PCIe (zero-copy).  The counterpart of the
+// reference's random-access reader (storage.cpp:320-341) for indexes larger
+// than HBM.
 struct Slab {
     uint32_t block, s0, ns; // slices [s0, s0+ns) of `block`
     uint64_t base;          // offset inside the staging buffer
@@ -157,6 +159,29 @@ std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n_docs, uint
                                             double median, double sigma, double p, int device,
                                             uint64_t block_lo = 0, uint64_t block_hi = ~0ull);
 
+// std::vector storage without value-initialisation (result buffers that a
+// device copy overwrites at once)
+template <typename T>
+struct NoInitAlloc : std::allocator<T> {
+    template <typename U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <typename U>
+    NoInitAlloc(const NoInitAlloc<U>&) {}
+    template <typename U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <typename U, typename... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <typename T>
+using RawVec = std::vector<T, NoInitAlloc<T>>;
+
 struct QueryResults {
     uint64_t n = 0;
     std::vector<uint32_t> ell, tau;
@@ -164,8 +189,8 @@ struct QueryResults {
     std::vector<int> status;
     std::vector<std::string> message;
     std::vector<uint64_t> hit_off, hit_n; // per query, into doc/score (after top_t)
-    std::vector<uint32_t> doc, score;
-    std::vector<uint8_t> scores; // dense, n x D x score_bytes
+    RawVec<uint32_t> doc, score;
+    RawVec<uint8_t> scores; // dense, n x D x score_bytes
     uint32_t score_bytes = 2;
     double ms_termize = 0, ms_gather = 0, ms_order = 0, ms_total = 0;
     uint32_t launches = 0; // kernels of ours launched by the batch

@@ -526,6 +526,41 @@ __global__ void make_keys_kernel(uint64_t m, const uint32_t* score, const uint32
     perm[i] = static_cast<uint32_t>(i);
 }
 
+// One ascending key for the whole batch order (query, score desc, name asc):
+// query id above the (score, name rank) key of make_keys_kernel.
+__global__ void make_qkeys_kernel(uint64_t m, const uint32_t* q, const uint32_t* score, const uint32_t* doc,
+                                  const uint32_t* rank, int rbits, int sbits, uint32_t smask, uint64_t* key,
+                                  uint32_t* perm) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    key[i] = (static_cast<uint64_t>(q[i]) << (sbits + rbits)) |
+             (static_cast<uint64_t>(~score[i] & smask) << rbits) | rank[doc[i]];
+    perm[i] = static_cast<uint32_t>(i);
+}
+
+// top_t on the device: hit i of the sorted batch (query q = its segment, rank
+// j inside it) is kept iff j < top_t, at out_start[q] + j (query.cpp:161-162);
+// seg_start / out_start are the exclusive scans of the per-query counts and
+// of min(count, top_t).
+__global__ void truncate_kernel(uint64_t m, uint64_t n, const uint64_t* seg_start, const uint64_t* out_start,
+                                uint64_t top_t, const uint32_t* perm, const uint32_t* doc, const uint32_t* score,
+                                uint32_t* out_doc, uint32_t* out_score) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    uint64_t lo = 0, hi = n; // seg_start[lo] <= i < seg_start[hi]
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (seg_start[mid] <= i)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const uint64_t j = i - seg_start[lo];
+    if (j >= top_t) return;
+    out_doc[out_start[lo] + j] = doc[perm[i]];
+    out_score[out_start[lo] + j] = score[perm[i]];
+}
+
 __global__ void gather_u32_kernel(uint64_t m, const uint32_t* perm, const uint32_t* src,
                                   uint32_t* dst) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -834,46 +869,84 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     }
 
     phase.begin("cobs.query.order");
-    // kernel 3: order hits by (query, score desc, name asc)
+    // kernel 3: order hits by (query, score desc, name asc): one radix sort
+    // of (query | ~score | name rank) keys with the hit index as the value,
+    // then the kept hits gathered -- all of them, or the first top_t of each
+    // query cut on the device so only those cross PCIe
     const uint64_t m = h_total;
+    std::vector<uint32_t> cnt(n);
+    uint64_t m_out = 0;
     if (want_hits && m > 0) {
         ws.key64.reserve(8 * m);
         ws.key64_alt.reserve(8 * m);
-        ws.key32.reserve(4 * m);
-        ws.key32_alt.reserve(4 * m);
         ws.perm.reserve(4 * m);
         ws.perm_alt.reserve(4 * m);
         ws.out_doc.reserve(4 * m);
         ws.out_score.reserve(4 * m);
-        int rbits = bits_for(D ? D - 1 : 0);
-        int sbits = nt_needed;
-        uint32_t smask = sbits >= 32 ? 0xffffffffu : ((1u << sbits) - 1u);
-        unsigned g = static_cast<unsigned>((m + 255) / 256);
-        make_keys_kernel<<<g, 256, 0, st>>>(m, ws.hit_score.as<uint32_t>(), ws.hit_doc.as<uint32_t>(),
-                                            ix.d_name_rank, rbits, smask, ws.key64.as<uint64_t>(),
-                                            ws.perm.as<uint32_t>());
-        COBS_CUDA(cudaGetLastError());
+        const int rbits = bits_for(D ? D - 1 : 0), sbits = nt_needed, qbits = bits_for(n ? n - 1 : 0);
+        const uint32_t smask = sbits >= 32 ? 0xffffffffu : ((1u << sbits) - 1u);
+        const unsigned g = static_cast<unsigned>((m + 255) / 256);
         cub::DoubleBuffer<uint64_t> k64(ws.key64.as<uint64_t>(), ws.key64_alt.as<uint64_t>());
         cub::DoubleBuffer<uint32_t> pv(ws.perm.as<uint32_t>(), ws.perm_alt.as<uint32_t>());
-        size_t tmp1 = 0, tmp2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp1, k64, pv, static_cast<int>(m), 0, rbits + sbits, st);
-        cub::DoubleBuffer<uint32_t> k32(ws.key32.as<uint32_t>(), ws.key32_alt.as<uint32_t>());
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp2, k32, pv, static_cast<int>(m), 0, bits_for(n), st);
-        ws.cub_tmp.reserve(std::max(tmp1, tmp2));
-        tmp1 = ws.cub_tmp.bytes;
-        COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp1, k64, pv, static_cast<int>(m), 0,
-                                                  rbits + sbits, st));
-        // stable secondary sort by query id
-        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_q.as<uint32_t>(), k32.Current());
-        tmp2 = ws.cub_tmp.bytes;
-        COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp2, k32, pv, static_cast<int>(m), 0,
-                                                  bits_for(n), st));
-        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_doc.as<uint32_t>(),
-                                             ws.out_doc.as<uint32_t>());
-        gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_score.as<uint32_t>(),
-                                             ws.out_score.as<uint32_t>());
+        if (qbits + sbits + rbits <= 64) {
+            make_qkeys_kernel<<<g, 256, 0, st>>>(m, ws.hit_q.as<uint32_t>(), ws.hit_score.as<uint32_t>(),
+                                                 ws.hit_doc.as<uint32_t>(), ix.d_name_rank, rbits, sbits, smask,
+                                                 ws.key64.as<uint64_t>(), ws.perm.as<uint32_t>());
+            COBS_CUDA(cudaGetLastError());
+            size_t tmp = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp, k64, pv, static_cast<int>(m), 0, qbits + sbits + rbits, st);
+            ws.cub_tmp.reserve(tmp);
+            tmp = ws.cub_tmp.bytes;
+            COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp, k64, pv, static_cast<int>(m), 0,
+                                                      qbits + sbits + rbits, st));
+            R.launches += 2;
+        } else { // (> 64 key bits) score+name sort, then a stable sort by query
+            ws.key32.reserve(4 * m);
+            ws.key32_alt.reserve(4 * m);
+            make_keys_kernel<<<g, 256, 0, st>>>(m, ws.hit_score.as<uint32_t>(), ws.hit_doc.as<uint32_t>(),
+                                                ix.d_name_rank, rbits, smask, ws.key64.as<uint64_t>(),
+                                                ws.perm.as<uint32_t>());
+            COBS_CUDA(cudaGetLastError());
+            size_t tmp1 = 0, tmp2 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp1, k64, pv, static_cast<int>(m), 0, rbits + sbits, st);
+            cub::DoubleBuffer<uint32_t> k32(ws.key32.as<uint32_t>(), ws.key32_alt.as<uint32_t>());
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp2, k32, pv, static_cast<int>(m), 0, qbits, st);
+            ws.cub_tmp.reserve(std::max(tmp1, tmp2));
+            tmp1 = ws.cub_tmp.bytes;
+            COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp1, k64, pv, static_cast<int>(m), 0,
+                                                      rbits + sbits, st));
+            gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_q.as<uint32_t>(), k32.Current());
+            tmp2 = ws.cub_tmp.bytes;
+            COBS_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.ptr, tmp2, k32, pv, static_cast<int>(m), 0, qbits,
+                                                      st));
+            R.launches += 4;
+        }
+        // per-query counts decide whether top_t shrinks what comes back
+        COBS_CUDA(cudaMemcpyAsync(cnt.data(), ws.hit_count.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        uint64_t kept = 0;
+        for (uint64_t i = 0; i < n; ++i) kept += (top_t > 0 && cnt[i] > top_t) ? top_t : cnt[i];
+        if (kept < m) { // cut every query to its first top_t on the device
+            std::vector<uint64_t> starts(2 * (n + 1), 0);
+            for (uint64_t i = 0; i < n; ++i) {
+                starts[i + 1] = starts[i] + cnt[i];
+                starts[n + 1 + i + 1] = starts[n + 1 + i] + std::min<uint64_t>(cnt[i], top_t);
+            }
+            ws.starts.reserve(8 * starts.size());
+            COBS_CUDA(cudaMemcpyAsync(ws.starts.ptr, starts.data(), 8 * starts.size(), cudaMemcpyHostToDevice, st));
+            truncate_kernel<<<g, 256, 0, st>>>(m, n, ws.starts.as<uint64_t>(), ws.starts.as<uint64_t>() + n + 1, top_t,
+                                               pv.Current(), ws.hit_doc.as<uint32_t>(), ws.hit_score.as<uint32_t>(),
+                                               ws.out_doc.as<uint32_t>(), ws.out_score.as<uint32_t>());
+            R.launches += 1;
+        } else {
+            gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_doc.as<uint32_t>(),
+                                                 ws.out_doc.as<uint32_t>());
+            gather_u32_kernel<<<g, 256, 0, st>>>(m, pv.Current(), ws.hit_score.as<uint32_t>(),
+                                                 ws.out_score.as<uint32_t>());
+            R.launches += 2;
+        }
         COBS_CUDA(cudaGetLastError());
-        R.launches += 4;
+        m_out = kept;
     }
     COBS_CUDA(cudaEventRecord(ev[3], st));
 
@@ -883,16 +956,15 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     R.ell.resize(n);
     R.tau.resize(n);
     R.skipped.resize(n);
-    std::vector<uint32_t> cnt(n);
     COBS_CUDA(cudaMemcpyAsync(R.ell.data(), ws.ell.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
     COBS_CUDA(cudaMemcpyAsync(R.tau.data(), ws.tau.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
     COBS_CUDA(cudaMemcpyAsync(R.skipped.data(), ws.skipped.ptr, 8 * n, cudaMemcpyDeviceToHost, st));
-    COBS_CUDA(cudaMemcpyAsync(cnt.data(), ws.hit_count.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
-    if (!keep && want_hits && m > 0) {
-        R.doc.resize(m);
-        R.score.resize(m);
-        COBS_CUDA(cudaMemcpyAsync(R.doc.data(), ws.out_doc.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
-        COBS_CUDA(cudaMemcpyAsync(R.score.data(), ws.out_score.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
+    if (!(want_hits && m > 0)) COBS_CUDA(cudaMemcpyAsync(cnt.data(), ws.hit_count.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (!keep && want_hits && m_out > 0) {
+        R.doc.resize(m_out); // (default-initialised: no zero fill before the copy)
+        R.score.resize(m_out);
+        COBS_CUDA(cudaMemcpyAsync(R.doc.data(), ws.out_doc.ptr, 4 * m_out, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaMemcpyAsync(R.score.data(), ws.out_score.ptr, 4 * m_out, cudaMemcpyDeviceToHost, st));
     }
     if (!keep && want_scores) {
         R.scores.resize(n * D * R.score_bytes);
@@ -906,11 +978,12 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     R.hit_off.resize(n);
     R.hit_n.resize(n);
     uint64_t o = 0;
+    const bool cut = m_out < m; // the device already kept only the first top_t per query
     for (uint64_t i = 0; i < n; ++i) {
         R.hit_off[i] = o;
         uint64_t c = want_hits ? cnt[i] : 0;
         R.hit_n[i] = keep ? 0 : ((top_t > 0 && c > top_t) ? top_t : c); // query.cpp:161-162
-        o += c;
+        o += cut ? R.hit_n[i] : c;
         if (R.ell[i] == 0) { // query.cpp:133-138
             R.status[i] = COBS_EDATA;
             R.message[i] = R.skipped[i] > 0
