@@ -2,11 +2,14 @@
 // procedural generator.  The HBM layout is described in DESIGN.md §3.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
 #include <numeric>
 #include <thread>
+
+#include <sys/mman.h>
 
 #include "index.hpp"
 #include "synth.h"
@@ -109,6 +112,52 @@ void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_
     }
     for (int b = 0; b < 2; ++b)
         if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // the pool is reused after return
+}
+
+void* result_alloc(size_t bytes) {
+    constexpr size_t kHuge = 2u << 20;
+    if (bytes < kHuge) {
+        void* p = std::malloc(std::max<size_t>(bytes, 1));
+        if (!p) throw std::bad_alloc();
+        return p;
+    }
+    const size_t len = (bytes + kHuge - 1) / kHuge * kHuge;
+    void* p = std::aligned_alloc(kHuge, len);
+    if (!p) throw std::bad_alloc();
+    madvise(p, len, MADV_HUGEPAGE); // best effort
+    return p;
+}
+void result_free(void* p) noexcept { std::free(p); }
+
+void d2h_staged(void* dst_host, const void* src_dev, uint64_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (bytes <= (4ull << 20) || is_pinned(dst_host)) {
+        COBS_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    StagePool& P = stage_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+    const uint8_t* src = static_cast<const uint8_t*>(src_dev);
+    uint8_t* dst = static_cast<uint8_t*>(dst_host);
+    const uint64_t nchunks = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](uint64_t c) {
+        const int b = static_cast<int>(c & 1);
+        P.buf[b].reserve(kStageBytes);
+        COBS_CUDA(cudaMemcpyAsync(P.buf[b].ptr, src + c * kStageBytes, std::min(kStageBytes, bytes - c * kStageBytes),
+                                  cudaMemcpyDeviceToHost, st));
+        COBS_CUDA(cudaEventRecord(done[b], st));
+    };
+    issue(0);
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int b = static_cast<int>(c & 1);
+        COBS_CUDA(cudaEventSynchronize(done[b]));
+        if (c + 1 < nchunks) issue(c + 1); // the next chunk's DMA runs while this one is copied out
+        const uint8_t* stage = P.buf[b].as<uint8_t>();
+        const uint64_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
+        host_parallel(len, 8ull << 20, [&](uint64_t lo, uint64_t hi) { std::memcpy(dst + off + lo, stage + lo, hi - lo); });
+    }
 }
 
 void d2h_unpitch(void* dst_host, const uint8_t* src_dev, uint64_t rows, uint32_t row_bytes, uint32_t pitch,

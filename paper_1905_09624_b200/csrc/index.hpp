@@ -137,6 +137,10 @@ struct DeviceIndex {
 // (the driver's own pageable path is one thread and a narrow 2D copy engine
 // path is slower still).  Pinned sources/destinations are copied directly.
 void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_t st);
+// Device -> pageable host through the same pinned pair, host threads copying
+// chunk i out while chunk i+1 is in flight (the driver's pageable D2H path
+// runs at ~2 GB/s into freshly allocated memory).  Synchronous.
+void d2h_staged(void* dst_host, const void* src_dev, uint64_t bytes, cudaStream_t st);
 // Rows [0, rows) of a pitched device matrix (row_bytes of each pitch-byte
 // row) into a packed host array: pitched 1D chunks D2H, un-pitched by host
 // threads (no narrow-row 2D copies).  Synchronous.
@@ -159,8 +163,14 @@ std::unique_ptr<DeviceIndex> synth_c5_index(uint64_t seed, uint64_t n_docs, uint
                                             double median, double sigma, double p, int device,
                                             uint64_t block_lo = 0, uint64_t block_hi = ~0ull);
 
+// Host memory for large result buffers: 2 MB aligned and advised for
+// transparent huge pages (the first touch of fresh 4 KB pages costs more than
+// the copy that fills them: ~0.3 s for 800 MB of hits).
+void* result_alloc(size_t bytes);
+void result_free(void* p) noexcept;
+
 // std::vector storage without value-initialisation (result buffers that a
-// device copy overwrites at once)
+// device copy overwrites at once), large ones on huge pages
 template <typename T>
 struct NoInitAlloc : std::allocator<T> {
     template <typename U>
@@ -170,6 +180,8 @@ struct NoInitAlloc : std::allocator<T> {
     NoInitAlloc() = default;
     template <typename U>
     NoInitAlloc(const NoInitAlloc<U>&) {}
+    T* allocate(size_t n) { return static_cast<T*>(result_alloc(n * sizeof(T))); }
+    void deallocate(T* p, size_t) noexcept { result_free(p); }
     template <typename U>
     void construct(U* p) noexcept {
         ::new (static_cast<void*>(p)) U;

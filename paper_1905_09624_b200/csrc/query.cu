@@ -960,16 +960,16 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
     COBS_CUDA(cudaMemcpyAsync(R.tau.data(), ws.tau.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
     COBS_CUDA(cudaMemcpyAsync(R.skipped.data(), ws.skipped.ptr, 8 * n, cudaMemcpyDeviceToHost, st));
     if (!(want_hits && m > 0)) COBS_CUDA(cudaMemcpyAsync(cnt.data(), ws.hit_count.ptr, 4 * n, cudaMemcpyDeviceToHost, st));
+    // large results: pinned staging + host threads (d2h_staged)
     if (!keep && want_hits && m_out > 0) {
         R.doc.resize(m_out); // (default-initialised: no zero fill before the copy)
         R.score.resize(m_out);
-        COBS_CUDA(cudaMemcpyAsync(R.doc.data(), ws.out_doc.ptr, 4 * m_out, cudaMemcpyDeviceToHost, st));
-        COBS_CUDA(cudaMemcpyAsync(R.score.data(), ws.out_score.ptr, 4 * m_out, cudaMemcpyDeviceToHost, st));
+        d2h_staged(R.doc.data(), ws.out_doc.ptr, 4 * m_out, st);
+        d2h_staged(R.score.data(), ws.out_score.ptr, 4 * m_out, st);
     }
     if (!keep && want_scores) {
         R.scores.resize(n * D * R.score_bytes);
-        COBS_CUDA(cudaMemcpyAsync(R.scores.data(), ws.scores.ptr, R.scores.size(),
-                                  cudaMemcpyDeviceToHost, st));
+        d2h_staged(R.scores.data(), ws.scores.ptr, R.scores.size(), st);
     }
     COBS_CUDA(cudaEventRecord(ev_end, st));
     COBS_CUDA(cudaStreamSynchronize(st));

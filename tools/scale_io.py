@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--dir", default="/tmp")
     ap.add_argument("--queries", type=int, default=1000)
     ap.add_argument("--skip-file", action="store_true")
+    ap.add_argument("--file-docs", type=int, default=70_000, help="documents of the C5 index written to disk")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "scale_io.json"))
     a = ap.parse_args()
     cfg = synth.CONFIGS["c5"]
@@ -50,14 +51,21 @@ def main():
         hits = int(r.hit_n.sum())
         dense[str(K)] = {"queries": a.queries, "hits": hits, "hits_per_query": hits / a.queries,
                          "ms_termize": r.ms_termize, "ms_gather": r.ms_gather, "ms_order": r.ms_order,
-                         "ms_call_wall": wall * 1e3,
+                         "ms_call_wall": wall * 1e3, "ms_total_events": r.ms_total,
                          "order_hits_per_s": hits / (r.ms_order / 1e3) if r.ms_order else None,
                          "order_share_of_kernels": r.ms_order / (r.ms_termize + r.ms_gather + r.ms_order)}
         print(K, dense[str(K)], flush=True)
     out["dense_hits"] = dense
     ref_batch = cb.query_batch_raw(view, qb, qo, 0.3, 10)
 
-    # ---- write the ~100 GB file, then the resident open ------------------
+    # ---- write the file, then the resident open ---------------------------
+    # (the GPU box's disk holds ~80 GB: the file leg uses --file-docs
+    # documents of the same C5 shape, ~0.99 GB per 1,000 documents)
+    if a.file_docs and a.file_docs != cfg.n_docs:
+        view.close()
+        view = cb.synth_c5(cfg.seed, a.file_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p)
+        ref_batch = cb.query_batch_raw(view, qb, qo, 0.3, 10)
+        out["file_docs"] = a.file_docs
     if not a.skip_file:
         path = os.path.join(a.dir, "c5_scale.cobs")
         free = shutil.disk_usage(a.dir).free
