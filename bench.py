@@ -323,7 +323,7 @@ def run_gpu(args):
     rank, world, local = world_info(args)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or "WORLD_SIZE" in os.environ:  # (a 1-rank torchrun still runs the NCCL exchange)
         import torch.distributed as dist
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (NVLS etc.) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -584,6 +584,26 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
                           "fill_hashes_per_s": cfg.k * windows / (f / 1e3),
                           "algo_bytes": int(lengths.sum()) + index_bytes,
                           "algo_gbs": (int(lengths.sum()) + index_bytes) / ((c + f) / 1e3) / 1e9}}
+    # Rooflines of the two passes against the measured HBM copy peak.  Neither
+    # is HBM-bound: the count's design traffic (corpus rolled twice, 8-byte
+    # keys written, re-sorted and read: 34 B per window) runs at a fraction of
+    # peak, bound by the shared-memory pipe of its dedup sets; the fill
+    # (corpus once + the matrix written and copied) is issue-bound on the
+    # IMAD pipe (XXH64's 64-bit multiplies).  ncu figures: committed captures.
+    peak, _ = measured_peak()
+    count_bytes = 34 * windows
+    fill_bytes = int(lengths.sum()) + 3 * index_bytes
+    out["roofline"] = {
+        "count": {"bound": "shared-memory pipe of the dedup sets (ncu L1/TEX 80 % busy), not HBM",
+                  "design_bytes": count_bytes, "achieved_gbs": count_bytes / (c / 1e3) / 1e9,
+                  "peak_gbs": peak, "frac": count_bytes / (c / 1e3) / 1e9 / peak,
+                  "ncu": "profiles/r2/count_ab.md (pc_dedup: L1/TEX 80.5 %, issue 48 %; hist issue 63 %)"},
+        "fill": {"bound": "issue (IMAD pipe: XXH64's 19 64-bit multiplies per window), not HBM",
+                 "design_bytes": fill_bytes, "achieved_gbs": fill_bytes / (f / 1e3) / 1e9,
+                 "peak_gbs": peak, "frac": fill_bytes / (f / 1e3) / 1e9 / peak,
+                 "issue_active_frac": 0.745,
+                 "ncu": "profiles/r1/build_fill_wave_c3_details.csv (slab_fill_kernel, one C3 wave: 74.5 % issue "
+                        "active, math-pipe throttle the top stall)"}}
     try:
         out["cpu_reference"] = cpu_reference_build(cfg, synth, BUILD_CPU_SAMPLE[name])
     except Exception as e:
