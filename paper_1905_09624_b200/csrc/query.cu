@@ -860,7 +860,9 @@ void query_batch_one(DeviceIndex& ix, const uint8_t* patterns, const uint64_t* o
         COBS_CUDA(cudaEventRecord(ev[2], st));
         COBS_CUDA(cudaMemcpyAsync(&h_total, ws.hit_total.ptr, 8, cudaMemcpyDeviceToHost, st));
         COBS_CUDA(cudaStreamSynchronize(st));
-        if (want_hits && h_total > hit_limit()) throw HitsOverflow{h_total}; // caller splits the batch
+        // (the limit queries free HBM -- a driver call -- so only for big hit counts)
+        if (want_hits && h_total > (std::getenv("COBS_HIT_LIMIT") ? 0ull : (1ull << 24)) && h_total > hit_limit())
+            throw HitsOverflow{h_total};
         if (h_total <= ws.hit_cap) break;
         ws.hit_cap = h_total + h_total / 8;
         ws.hit_q.reserve(4 * ws.hit_cap);
