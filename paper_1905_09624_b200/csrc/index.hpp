@@ -118,6 +118,7 @@ struct DeviceIndex {
     uint64_t sum_row_bytes = 0; // sum_b row_bytes_b
     uint64_t column_offset = 0; // block shard: file column of this index's first document
     bool evict_first = false;   // payload far larger than L2
+    uint64_t free_hbm_seen = 0; // the last free-HBM reading of a query batch (0: none yet)
     std::mutex mu;
     QueryWorkspace ws;
     std::unique_ptr<HostStream> hs; // non-null: host-resident (streaming) mode
