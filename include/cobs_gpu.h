@@ -207,7 +207,8 @@ uint64_t cobs_gpu_results_h2d_index_bytes(const cobs_gpu_results* r);
  * the host-resident (pinned) payload directly over PCIe (zero-copy: only the
  * addressed rows), 2 = the host-resident payload streamed through HBM staging
  * buffers (the whole payload per batch).  All compute the same scores and
- * hits (query.cpp:49-89); h2d_index_bytes counts the index bytes moved. */
+ * hits (query.cpp:49-89);
+ * h2d_index_bytes counts the index bytes moved. */
 uint32_t cobs_gpu_results_gather_path(const cobs_gpu_results* r);
 void cobs_gpu_results_free(cobs_gpu_results* r);
 

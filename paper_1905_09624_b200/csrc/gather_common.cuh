@@ -1,5 +1,5 @@
 // Bit-sliced counting helpers shared by the row-gather kernels (query.cu:
-// gather_kernel, tiled.cu: tile_kernel).  The reference counts with a
+// gather_kernel).  The reference counts with a
 // 256 x 8 expand table per AND byte (query.cpp:25-45,74-81); here 32
 // documents' counts live as bit planes of one 32-bit word per lane and
 // masks are added with carry-save (Harley-Seal) adders.
@@ -93,6 +93,67 @@ __device__ __forceinline__ uint32_t csa16(const uint32_t* v, uint32_t& ones, uin
     csa(eightsB, fours, fours, foursA, foursB);
     csa(sixteens, eights, eights, eightsA, eightsB);
     return sixteens;
+}
+
+// Where a gather writes a finished (query, slice)'s results: dense scores
+// and/or hits (document order within the slice; kernel 3 orders them).
+struct EmitArgs {
+    void* scores; // dense [n][D] (uint16 when NT <= 16, else uint32) or null
+    uint64_t D;
+    int want_hits;
+    uint32_t* hit_count; // per query
+    unsigned long long* hit_total;
+    uint64_t hit_cap;
+    uint32_t* hit_q;
+    uint32_t* hit_doc;
+    uint32_t* hit_score;
+};
+
+// The 32 documents of a lane (global columns gdoc0.., `valid` of them real)
+// with counts F: dense scores, then F >= tau bit-sliced over all 32 at once,
+// compacted with a warp scan and one atomic per warp (query.cpp:83-88).
+template <int NT>
+__device__ __forceinline__ void emit_slice(const EmitArgs& a, uint64_t qi, uint64_t gdoc0, uint32_t valid,
+                                           uint32_t tau, const uint32_t (&F)[NT], uint32_t lane) {
+    if (a.scores) {
+        if (NT <= 16) {
+            uint16_t* row = static_cast<uint16_t*>(a.scores) + qi * a.D + gdoc0;
+            for (int i = 0; i < 32; ++i)
+                if ((valid >> i) & 1u) row[i] = static_cast<uint16_t>(extract<NT>(F, i));
+        } else {
+            uint32_t* row = static_cast<uint32_t*>(a.scores) + qi * a.D + gdoc0;
+            for (int i = 0; i < 32; ++i)
+                if ((valid >> i) & 1u) row[i] = extract<NT>(F, i);
+        }
+    }
+    if (!a.want_hits) return;
+    uint32_t hits = ge_mask<NT>(F, tau) & valid;
+    uint32_t cnt = __popc(hits);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    unsigned long long base = 0;
+    if (lane == 31) {
+        base = atomicAdd(a.hit_total, (unsigned long long)total);
+        atomicAdd(a.hit_count + qi, total);
+    }
+    base = __shfl_sync(0xffffffffu, base, 31);
+    uint64_t idx = base + incl - cnt;
+    while (hits) {
+        int i = __ffs(hits) - 1;
+        hits &= hits - 1;
+        if (idx < a.hit_cap) {
+            a.hit_q[idx] = static_cast<uint32_t>(qi);
+            a.hit_doc[idx] = static_cast<uint32_t>(gdoc0 + i);
+            a.hit_score[idx] = extract<NT>(F, i);
+        }
+        ++idx;
+    }
 }
 
 } // namespace cobsg

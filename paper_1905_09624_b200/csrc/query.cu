@@ -472,46 +472,8 @@ __global__ void __launch_bounds__(256, COBS_GATHER_MINB) gather_kernel(GatherArg
         }
     }
 
-    if (a.scores) {
-        if (NT <= 16) {
-            uint16_t* row = static_cast<uint16_t*>(a.scores) + qi * a.D + gdoc0;
-            for (int i = 0; i < 32; ++i)
-                if ((valid >> i) & 1u) row[i] = static_cast<uint16_t>(extract<NT>(F, i));
-        } else {
-            uint32_t* row = static_cast<uint32_t*>(a.scores) + qi * a.D + gdoc0;
-            for (int i = 0; i < 32; ++i)
-                if ((valid >> i) & 1u) row[i] = extract<NT>(F, i);
-        }
-    }
-    if (!a.want_hits) return;
-    // Bit-sliced F >= tau over all 32 documents of the lane at once.
-    uint32_t hits = ge_mask<NT>(F, tau) & valid;
-    uint32_t cnt = __popc(hits);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) return;
-    unsigned long long base = 0;
-    if (lane == 31) {
-        base = atomicAdd(a.hit_total, (unsigned long long)total);
-        atomicAdd(a.hit_count + qi, total);
-    }
-    base = __shfl_sync(0xffffffffu, base, 31);
-    uint64_t idx = base + incl - cnt;
-    while (hits) {
-        int i = __ffs(hits) - 1;
-        hits &= hits - 1;
-        if (idx < a.hit_cap) {
-            a.hit_q[idx] = static_cast<uint32_t>(qi);
-            a.hit_doc[idx] = static_cast<uint32_t>(gdoc0 + i);
-            a.hit_score[idx] = extract<NT>(F, i);
-        }
-        ++idx;
-    }
+    const EmitArgs e{a.scores, a.D, a.want_hits, a.hit_count, a.hit_total, a.hit_cap, a.hit_q, a.hit_doc, a.hit_score};
+    emit_slice<NT>(e, qi, gdoc0, valid, tau, F, lane);
 }
 
 // ---- kernel 3 helpers ---------------------------------------------------

@@ -18,10 +18,14 @@ from workloads import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--queries", type=int, default=100_000)
+ap.add_argument("--repeat", type=int, default=1)
 a = ap.parse_args()
 cfg = synth.CONFIGS["c5"]
 view = cb.synth_c5(cfg.seed, cfg.n_docs, cfg.block_size, cfg.c5_median, cfg.c5_sigma, cfg.p)
 qb, qo = synth.queries(cfg, np.arange(a.queries, dtype=np.uint64))
-r = cb.query_batch_raw(view, qb, qo, cfg.K)
-print("gather ms %.2f, row bytes %d, %.1f GB/s" % (r.ms_gather, r.row_bytes, r.row_bytes / r.ms_gather / 1e6))
+for _ in range(a.repeat):
+    r = cb.query_batch_raw(view, qb, qo, cfg.K)
+    print("gather ms %.2f (path %d, %d launches), row bytes %d, %.1f GB/s algorithmic, hits %d"
+          % (r.ms_gather, r.gather_path, r.launches, r.row_bytes, r.row_bytes / r.ms_gather / 1e6,
+             int(r.hit_n.sum())), flush=True)
 view.close()
