@@ -4,6 +4,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            -Xcudafe --diag_suppress=177
+NVFLAGS += $(EXTRA)  # A/B builds: make lib EXTRA=-DCOBS_...=...
 SRC := paper_1905_09624_b200/csrc
 OUT := paper_1905_09624_b200/_lib
 OBJS := $(OUT)/host.o $(OUT)/frontend.o $(OUT)/index.o $(OUT)/query.o $(OUT)/build.o $(OUT)/merge.o \

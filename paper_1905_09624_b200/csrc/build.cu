@@ -97,15 +97,105 @@ __device__ __forceinline__ void roll_windows(const uint8_t* sb, uint64_t j0, uin
     }
 }
 
+// ---- packed rolling for 2-bit DNA codes (the count pass's hot loop) ----
+//
+// 16 bases enter at once: their bytes become 2-bit codes four at a time
+// (one multiply packs a word's four codes), and three shift registers hold
+// the recent bases -- forward codes newest-lowest (R, 128 bits), complement
+// codes newest-highest (T, 128 bits: reverse-complement codes read out
+// without any per-base reversal) and a 1-bit-per-base non-ACGT mask (Bm).
+// Each of the 16 windows ending in the chunk is then a constant-shift
+// extract of R and T (funnel shifts) and a mask test of Bm: ~13 integer ops
+// per window instead of a 64-bit shift/or/and chain per byte.
+struct U128 {
+    uint64_t hi, lo;
+};
+// low 64 bits of x >> s (0 <= s < 128)
+__device__ __forceinline__ uint64_t shr128(const U128& x, uint32_t s) {
+    if (s == 0) return x.lo;
+    if (s < 64) return (x.lo >> s) | (x.hi << (64 - s));
+    return x.hi >> (s - 64);
+}
+// codes of 4 A/C/G/T bytes packed into 8 bits, the first byte most significant
+__device__ __forceinline__ uint32_t pack4(uint32_t w) {
+    const uint32_t c = ((w >> 1) ^ (w >> 2)) & 0x03030303u; // base_code per byte
+    return (c * 0x40100401u) >> 24;
+}
+// 4 bits: bit 3 = byte 0 ... bit 0 = byte 3 is not one of A, C, G, T
+__device__ __forceinline__ uint32_t bad4(uint32_t w) {
+    const uint32_t c = ((w >> 1) ^ (w >> 2)) & 0x03030303u;
+    const uint32_t sel = (c | (c >> 4)) & 0x00ff00ffu; // nibble k = code of byte k
+    const uint32_t expect = __byte_perm(0x54474341u, 0u, (sel & 0xffu) | ((sel >> 8) & 0xff00u));
+    const uint32_t x = expect ^ w; // nonzero bytes: not the letter of their own code
+    if (x == 0u) return 0u;
+    const uint32_t nz = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+    return (((nz >> 7) * 0x08040201u) >> 24) & 0xfu;
+}
+
+template <int QC, typename F>
+__device__ __forceinline__ void roll_range_packed(const uint8_t* sb, uint64_t j0, uint64_t j1, uint32_t q_rt,
+                                                  bool canonical, F&& f) {
+    const uint32_t q = QC ? QC : q_rt;
+    const uint64_t mask = q >= 32 ? ~0ull : ((1ull << (2 * q)) - 1);
+    const uint64_t qmask = q >= 64 ? ~0ull : ((1ull << q) - 1);
+    const uint64_t end = j1 + q - 1, first = j0 + q - 1; // bytes [j0, end); windows end at >= first
+    U128 R{0, 0}, T{0, 0};
+    uint64_t Bm = 0;
+    uint64_t i = j0;
+    // window ending at byte e (pushed t bytes ago): emit if e >= first
+    auto emit = [&](uint64_t e, uint32_t t) {
+        if (e < first) return;
+        const bool ok = ((Bm >> t) & qmask) == 0;
+        uint64_t code = shr128(R, 2 * t) & mask;
+        if (canonical) { // min(gram, revcomp) bytewise == min of the codes
+            const uint64_t rc = shr128(T, 128 - 2 * q - 2 * t) & mask;
+            code = rc < code ? rc : code;
+        }
+        f(e - (q - 1), ok, code);
+    };
+    auto push1 = [&](uint32_t c) {
+        const uint32_t b = base_code(c);
+        R.hi = (R.hi << 2) | (R.lo >> 62);
+        R.lo = (R.lo << 2) | b;
+        T.lo = (T.lo >> 2) | (T.hi << 62);
+        T.hi = (T.hi >> 2) | (static_cast<uint64_t>(3u - b) << 62);
+        Bm = (Bm << 1) | (acgt_bit(c) ^ 1u);
+        emit(i, 0);
+        ++i;
+    };
+    while (i < end && (reinterpret_cast<uintptr_t>(sb + i) & 15u)) push1(__ldg(sb + i));
+    while (i + 16 <= end) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(sb + i));
+        const uint32_t P = (pack4(v.x) << 24) | (pack4(v.y) << 16) | (pack4(v.z) << 8) | pack4(v.w);
+        uint32_t rp = __brev(P); // complement codes, first base lowest
+        rp = ~(((rp >> 1) & 0x55555555u) | ((rp & 0x55555555u) << 1));
+        const uint32_t bad = (bad4(v.x) << 12) | (bad4(v.y) << 8) | (bad4(v.z) << 4) | bad4(v.w);
+        R.hi = (R.hi << 32) | (R.lo >> 32);
+        R.lo = (R.lo << 32) | P;
+        T.lo = (T.lo >> 32) | (T.hi << 32);
+        T.hi = (T.hi >> 32) | (static_cast<uint64_t>(rp) << 32);
+        Bm = (Bm << 16) | bad;
+        i += 16;
+#pragma unroll
+        for (int t = 15; t >= 0; --t) emit(i - 1 - static_cast<uint32_t>(t), static_cast<uint32_t>(t));
+    }
+    while (i < end) push1(__ldg(sb + i));
+}
+
 // roll_windows over a long range with 16-byte loads: the segment bytes
 // [j0, j1 + q - 1) are pushed in order (aligned uint4 loads for the body,
 // bytes at the ragged ends), f(j, dna, code) after every complete window j
-// in [j0, j1).  Only for q <= 32.
-template <int QC, int UNROLL = 4, int SB = 0, typename F>
+// in [j0, j1).  Only for q <= 32.  PACKED: 2-bit DNA codes 16 bases at a
+// time (roll_range_packed; small callbacks only -- it inlines f 16 times).
+template <int QC, int UNROLL = 4, int SB = 0, bool PACKED = false, typename F>
 __device__ __forceinline__ void roll_range(const uint8_t* sb, uint64_t j0, uint64_t j1, uint32_t q_rt,
                                            bool canonical, F&& f, const uint8_t* symtab = nullptr) {
     const uint32_t q = QC ? QC : q_rt;
     if (j1 <= j0) return;
+    if constexpr (PACKED && SB == 0) {
+        roll_range_packed<QC>(sb, j0, j1, q, canonical, f);
+        return;
+    }
     // SB > 0: small-alphabet symbol codes (non-canonical raw bytes), else 2-bit DNA codes
     typename std::conditional<SB == 0, Roller, SymRoller<SB ? SB : 1>>::type R = [&] {
         if constexpr (SB == 0) return Roller(q);
@@ -201,7 +291,10 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
 // global atomic per (chunk, bucket)), scattered into a key buffer, and every
 // bucket is deduplicated by one CTA in a shared-memory set.  Exact: a code
 // lands in exactly one bucket, and equal codes always in the same one.
-constexpr uint32_t kPcRunsPerThread = 16; // consecutive runs one thread rolls through
+#ifndef COBS_PC_RUNS
+#define COBS_PC_RUNS 16
+#endif
+constexpr uint32_t kPcRunsPerThread = COBS_PC_RUNS; // consecutive runs one thread rolls through
 constexpr uint32_t kPcRuns = 256 * kPcRunsPerThread; // runs (x kBRun windows) per chunk
 constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in shared memory
 constexpr uint32_t kPcMaxSlots = 16384; // largest dedup set (128 KB of shared memory)
@@ -237,6 +330,10 @@ __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
 }
 
 constexpr int kSymBits = 5;                  // symbol codes: <= 32 distinct byte values, q <= 12
+#ifndef COBS_PC_PACKED
+#define COBS_PC_PACKED 1
+#endif
+constexpr bool kPcPacked = COBS_PC_PACKED != 0; // 2-bit codes rolled 16 bases at a time (roll_range_packed)
 constexpr uint32_t kSupLog2 = 5;             // two-level scatter: <= 32 super-buckets per document (A/B: 64 and 256 slower)
 constexpr uint32_t kSup = 1u << kSupLog2;
 __device__ __forceinline__ uint32_t pc_super_shift(const PcDoc& D) { // bucket >> this = super-bucket
@@ -271,8 +368,9 @@ __device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uin
         const uint64_t len = a.seg_off[s + 1] - a.seg_off[s];
         const uint64_t W = len >= q ? len - q + 1 : 0;
         const uint64_t gend = min(ge, a.seg_rbase[s + 1]);
-        roll_range<QC, 4, SB>(a.seqs + a.seg_off[s], (g - rb) * kBRun, min(W, (gend - rb) * kBRun), q,
-                              a.canonical != 0, [&](uint64_t, bool dna, uint64_t code) { f(dna, code); }, symtab);
+        roll_range<QC, 4, SB, kPcPacked>(a.seqs + a.seg_off[s], (g - rb) * kBRun, min(W, (gend - rb) * kBRun), q,
+                                         a.canonical != 0, [&](uint64_t, bool dna, uint64_t code) { f(dna, code); },
+                                         symtab);
         g = gend;
     }
 }

@@ -1,14 +1,9 @@
 #!/bin/bash
-# A/B build timing on one box: tools/ab_build.sh <libA> <libB> <configs...>
-# (alternates the two libraries twice per config; prints count/fill ms)
-A=$1; B=$2; shift 2
-for cfg in "$@"; do
-  for rep in 1 2; do
-    for L in "$A" "$B"; do
-      COBS_GPU_LIB=$L python tools/config_runs.py $cfg --build-only --repeat 2 --out /tmp/ab.json > /tmp/ab.log 2>&1
-      python -c "
-import json,sys; r=json.load(open('/tmp/ab.json'))[0]['build']
-print('$cfg', '$(basename $L)', 'count %.1f fill %.1f total %.1f' % (r['ms_count'], r['ms_fill'], r['ms_total_call']))"
-    done
-  done
+# A/B of compile-time build knobs on one box: tools/ab_build.sh "-DCOBS_X=1" "-DCOBS_X=2" ...
+# (rebuilds the library per variant; C3 by default, CFG=c2|c4 to change)
+for v in "$@"; do
+  echo "== $v"
+  touch paper_1905_09624_b200/csrc/build.cu
+  make -j8 lib EXTRA="$v" > /dev/null 2>&1 || { echo "build failed"; continue; }
+  COBS_BUILD_DEBUG=1 python tools/config_runs.py ${CFG:-c3} --build-only --repeat 4 --out /tmp/ab.json 2>&1 | grep -E "count .* ms|ms_fill" | tail -3 | cut -c1-300
 done
