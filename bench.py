@@ -652,7 +652,8 @@ def run_gpu_blocks(args, rank, world, local, dist):
     import torch
     import paper_1905_09624_b200 as cb
     from workloads import synth
-    from paper_1905_09624_b200.dist import flat_hits, gather_block_hits, name_ranks, reduce_max, shard_range
+    from paper_1905_09624_b200.dist import (all_gather_arrays, flat_hits, gather_block_hits, name_ranks, reduce_max,
+                                            shard_range)
     if args.config != "c5":
         raise SystemExit("--shard blocks serves the compact C5 index")
     cfg = c5_config(args)
@@ -665,19 +666,16 @@ def run_gpu_blocks(args, rank, world, local, dist):
     stream = torch.cuda.Stream(device=local)
     view.set_stream(stream.cuda_stream)
     off = view.column_offset()
-    nr = None
-    # names of the C5 documents are zero-padded "docNNNNNN" of their draw
-    # index; rank 0 needs every column's name rank: from the full header
-    # order (term_count, name) -- the shard views know their own names only,
-    # so gather them once (setup, untimed)
-    from paper_1905_09624_b200.dist import all_gather_arrays
-    my_names = view.doc_names()
-    codes = np.array([int(n[3:]) for n in my_names], np.int64)  # "doc%06d" -> draw index
-    parts = all_gather_arrays([codes], f"cuda:{local}")
+    # rank 0 ranks every column's name (the merge's tie-break); each shard
+    # knows its own columns' names only -- C5 names are "doc" + the zero-padded
+    # draw index, so the draw indices are gathered once (setup, untimed)
+    ids = np.array([int(nm[3:]) for nm in view.doc_names()], np.int64)
+    parts = all_gather_arrays([ids], f"cuda:{local}")
+    name_rank = None
     if rank == 0:
-        all_codes = np.concatenate([p[0] for p in parts])
         width = max(6, len(str(cfg.n_docs - 1)))
-        nr = name_ranks([b"doc" + str(int(c)).zfill(width).encode() for c in all_codes])
+        name_rank = name_ranks([b"doc" + str(int(c)).zfill(width).encode()
+                                for c in np.concatenate([p[0] for p in parts])])
     qb, qo = synth.queries(cfg)
     n = len(qo) - 1
     dev = f"cuda:{local}"
@@ -685,7 +683,7 @@ def run_gpu_blocks(args, rank, world, local, dist):
     def step():
         r = cb.query_batch_raw(view, qb, qo, cfg.K)
         hn, cols, sc = flat_hits(r)
-        merged = gather_block_hits(hn, cols + off, sc, nr, 0, dev)
+        merged = gather_block_hits(hn, cols + off, sc, name_rank, 0, dev)
         return r, merged
 
     for _ in range(args.warmup):
