@@ -299,6 +299,8 @@ constexpr uint32_t kPcRuns = 256 * kPcRunsPerThread; // runs (x kBRun windows) p
 constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in shared memory
 constexpr uint32_t kPcMaxSlots = 16384; // largest dedup set (128 KB of shared memory)
 constexpr uint64_t kPcTarget = 4096;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
+constexpr uint64_t kPcTargetDirect = 4096; // the same for the fingerprint sets
+constexpr uint32_t kPcMaxSlotsFp = 32768;  // largest fingerprint set (128 KB of shared memory)
                                         // (A/B with 1x-mean sets: 1,024 / 2,048 / 4,096 -> C3 count 1.81 / 1.65 / 1.61 s)
 
 struct PcDoc {
@@ -310,6 +312,8 @@ struct PcDoc {
     uint32_t shift;          // 64 - log2(nbk); 64 = a single bucket
     uint32_t doc;            // global document index
     uint32_t sb0;            // two-level scatter: first super-bucket (wave-relative prefix)
+    uint32_t tpr;            // runs per thread in this document's chunks (a chunk = 256 x tpr runs)
+    uint64_t cc0;            // direct scatter: its (chunk, bucket) count matrix in chunk_cnt
 };
 
 struct PcArgs {
@@ -322,7 +326,10 @@ struct PcArgs {
     unsigned long long* keys; // code + 1, grouped by bucket
     unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
     uint32_t* chunk_sup;      // two-level: per (chunk, super-bucket) key counts [chunk][kSup], or null
+    uint32_t* chunk_cnt;      // direct: per (chunk, bucket) key counts at cc0 + local chunk x nbk, or null
     const uint8_t* symtab;    // SB > 0: byte -> symbol index (256 entries)
+    int mixed;                // keys are mix_code(code) (fingerprint dedup), else code + 1
+    int st_hint;              // direct scatter key stores: 0 plain, 1 L2 evict_last, 2 L2 evict_normal (A/B)
 };
 
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
@@ -354,14 +361,20 @@ __device__ __forceinline__ uint32_t pc_chunk_doc(const PcDoc* docs, uint32_t n, 
     return lo;
 }
 
+// runs [r0, r1) of chunk c of document D (256 threads x D.tpr runs)
+__device__ __forceinline__ void pc_chunk_runs(const PcDoc& D, uint64_t c, uint64_t& r0, uint64_t& r1) {
+    r0 = D.run_lo + (c - D.chunk0) * (256ull * D.tpr);
+    r1 = min(D.run_hi, r0 + static_cast<uint64_t>(256ull * D.tpr));
+}
+
 // f(dna, code) for every window of the chunk's runs; each thread rolls
-// through kPcRunsPerThread consecutive runs (256 threads per CTA)
+// through D.tpr consecutive runs (256 threads per CTA)
 template <int QC, int SB = 0, typename F>
 __device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uint64_t r0, uint64_t r1, F&& f,
                                            const uint8_t* symtab = nullptr) {
     const uint32_t q = QC ? QC : a.q;
-    uint64_t g = r0 + static_cast<uint64_t>(threadIdx.x) * kPcRunsPerThread;
-    const uint64_t ge = min(r1, g + kPcRunsPerThread);
+    uint64_t g = r0 + static_cast<uint64_t>(threadIdx.x) * D.tpr;
+    const uint64_t ge = min(r1, g + static_cast<uint64_t>(D.tpr));
     while (g < ge) {
         const uint64_t s = find_seg_in(a, g, D.seg_lo, D.seg_hi);
         const uint64_t rb = a.seg_rbase[s];
@@ -394,7 +407,8 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
         if (local)
             for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_hist[j] = 0;
         __syncthreads();
-        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        uint64_t r0, r1;
+        pc_chunk_runs(D, c, r0, r1);
         uint32_t bad = 0;
         pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
             if (!dna) { // canonical: skipped (termizer.cpp:113-116); else needs the byte path
@@ -409,9 +423,14 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
         }, s_sym);
         if (bad) atomicAdd(&s_bad, (unsigned long long)bad);
         __syncthreads();
-        if (local)
-            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x)
-                if (s_hist[j]) atomicAdd(&p.bucket_cnt[D.bucket0 + j], s_hist[j]);
+        if (local) {
+            uint32_t* cc = p.chunk_cnt ? p.chunk_cnt + D.cc0 + (c - D.chunk0) * D.nbk : nullptr;
+            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) {
+                const uint32_t h = s_hist[j];
+                if (h) atomicAdd(&p.bucket_cnt[D.bucket0 + j], h);
+                if (cc) cc[j] = h; // the direct scatter's reservation sizes
+            }
+        }
         if (local && p.chunk_sup) { // the two-level scatter's per-chunk super-bucket counts
             const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
             if (threadIdx.x < nsb) {
@@ -435,7 +454,8 @@ __global__ void __launch_bounds__(256) pc_scatter_kernel(PcArgs p) {
         if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
         __syncthreads();
         const PcDoc D = p.docs[s_doc];
-        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        uint64_t r0, r1;
+        pc_chunk_runs(D, c, r0, r1);
         if (D.nbk > kPcHist) { // very large document: one global cursor atomic per key
             pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
                 if (!dna) return;
@@ -507,7 +527,8 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
         if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
         __syncthreads();
         const PcDoc D = p.docs[s_doc];
-        const uint64_t r0 = D.run_lo + (c - D.chunk0) * kPcRuns, r1 = min(D.run_hi, r0 + kPcRuns);
+        uint64_t r0, r1;
+        pc_chunk_runs(D, c, r0, r1);
         const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
         const bool counted = p.chunk_sup && D.nbk <= kPcHist; // the histogram pass left the counts
         if (threadIdx.x < kSup) s_cnt[threadIdx.x] = 0;
@@ -525,8 +546,9 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
         __syncthreads();
         pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
             if (!dna) return;
-            const uint32_t sb = pc_bucket(code, D.shift) >> sbs;
-            p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = code + 1ull;
+            const uint64_t m = mix_code(code);
+            const uint32_t sb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(m >> D.shift)) >> sbs;
+            p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = p.mixed ? m : code + 1ull;
         }, s_sym);
     }
 }
@@ -540,7 +562,7 @@ constexpr uint32_t kFinPer = kFinTile / 256; // keys per thread per tile
 __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs, const uint32_t* sup_doc,
                                                                uint64_t nsup, const uint32_t* off,
                                                                const unsigned long long* keys_a,
-                                                               unsigned long long* keys_b) {
+                                                               unsigned long long* keys_b, int mixed) {
     constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
     __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB];
     __shared__ unsigned long long s_sorted[kFinTile];
@@ -566,8 +588,9 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
 #pragma unroll
             for (uint32_t u = 0; u < kFinPer; ++u) {
                 lr[u] = 0;
-                if (kv[u]) {
-                    const uint32_t lb = pc_bucket(kv[u] - 1ull, D.shift) & (bps - 1u);
+                if (threadIdx.x + u * blockDim.x < n) {
+                    const uint32_t lb = (mixed ? (D.shift >= 64 ? 0u : static_cast<uint32_t>(kv[u] >> D.shift))
+                                               : pc_bucket(kv[u] - 1ull, D.shift)) & (bps - 1u);
                     lr[u] = lb | (atomicAdd(&s_cnt[lb], 1u) << 8);
                 }
             }
@@ -589,7 +612,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
             __syncthreads();
 #pragma unroll
             for (uint32_t u = 0; u < kFinPer; ++u)
-                if (kv[u]) {
+                if (threadIdx.x + u * blockDim.x < n) {
                     const uint32_t pos = s_start[lr[u] & 0xffu] + (lr[u] >> 8);
                     s_sorted[pos] = kv[u];
                     s_lb[pos] = static_cast<uint8_t>(lr[u] & 0xffu);
@@ -602,6 +625,247 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
             __syncthreads();
             for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] += s_cnt[t];
         }
+    }
+}
+
+// ---- direct scatter + fingerprint dedup (one key round trip) ----------
+//
+// The histogram pass leaves every (chunk, bucket) count; a chunk reserves
+// each bucket's run with one cursor atomic and writes its keys there.  Chunks
+// are sized per document (256 x D.tpr runs) so a (chunk, bucket) run is a
+// few hundred keys -- whole DRAM sectors -- even at thousands of buckets.
+// Keys are stored mixed (mix_code is a bijection, so distinctness is kept):
+// the bucket is the key's top bits and the dedup needs no re-mix.
+template <int QC, int SB = 0>
+__global__ void __launch_bounds__(256) pc_scatter_direct_kernel(PcArgs p) {
+    extern __shared__ uint32_t pc_smem[];
+    uint32_t* s_cnt = pc_smem;            // <= kPcHist
+    uint32_t* s_base = pc_smem + kPcHist; // <= kPcHist
+    __shared__ uint32_t s_doc;
+    __shared__ uint8_t s_sym[256];
+    if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
+        __syncthreads();
+        const PcDoc D = p.docs[s_doc];
+        uint64_t r0, r1;
+        pc_chunk_runs(D, c, r0, r1);
+        const uint32_t* cc = p.chunk_cnt + D.cc0 + (c - D.chunk0) * D.nbk;
+        for (uint32_t j0 = threadIdx.x; j0 < D.nbk; j0 += 4 * blockDim.x) { // 4 reservations in flight
+            uint32_t n[4], base[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * blockDim.x;
+                n[u] = j < D.nbk ? cc[j] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (n[u]) base[u] = atomicAdd(&p.cursor[D.bucket0 + j0 + u * blockDim.x], n[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * blockDim.x;
+                if (n[u]) s_base[j] = base[u];
+                if (j < D.nbk) s_cnt[j] = 0;
+            }
+        }
+        __syncthreads();
+        pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
+            if (!dna) return;
+            const uint64_t m = mix_code(code);
+            const uint32_t b = D.shift >= 64 ? 0u : static_cast<uint32_t>(m >> D.shift);
+            unsigned long long* dst = p.keys + s_base[b] + atomicAdd(&s_cnt[b], 1u);
+            if (p.st_hint == 0) {
+                *dst = m;
+            } else {
+                uint64_t pol;
+                if (p.st_hint == 1)
+                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                else
+                    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(dst), "l"(m), "l"(pol) : "memory");
+            }
+        }, s_sym);
+    }
+}
+
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(phase)
+                 : "memory");
+}
+
+// key i of a bucket staged in shared memory (SMEM) or read from global memory
+template <bool SMEM>
+__device__ __forceinline__ unsigned long long dd_key(uint32_t s_base, const unsigned long long* g, uint32_t i) {
+    if constexpr (SMEM) {
+        unsigned long long v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(s_base + 8u * i));
+        return v;
+    } else {
+        return __ldg(g + i);
+    }
+}
+
+// One probe of a key of the fingerprint set (see pc_dedup_fp_kernel):
+// returns true once the key is settled (new -> ++mine, duplicate, or
+// stuck = every group full).
+struct DdKey {
+    unsigned long long m;
+    uint32_t i, probes;
+};
+template <bool SMEM>
+__device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t s_keys,
+                                         const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
+    uint32_t fp = static_cast<uint32_t>(k.m >> 16) & ~imask;
+    fp = fp ? fp : imask + 1u;
+    const uint32_t gaddr = sg + 16u * ((static_cast<uint32_t>(k.m) + k.probes) & gmask);
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(gaddr));
+    // slot j holds this fingerprint iff (slot ^ fp) <= imask (an empty slot never does: fp > imask)
+    if (((v.x ^ fp) <= imask) | ((v.y ^ fp) <= imask) | ((v.z ^ fp) <= imask) | ((v.w ^ fp) <= imask)) {
+        const uint32_t sl[4] = {v.x, v.y, v.z, v.w}; // (rare: a duplicate, or a fingerprint accident)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if ((sl[j] ^ fp) <= imask && dd_key<SMEM>(s_keys, g_keys, sl[j] & imask) == k.m) return true;
+    }
+    const uint32_t occ = (v.x != 0u) + (v.y != 0u) + (v.z != 0u) + (v.w != 0u); // occupied slots are a prefix
+    if (occ < 4u) {
+        uint32_t cur;
+        asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(cur) : "r"(gaddr + 4u * occ), "r"(0u), "r"(fp | k.i)
+                     : "memory");
+        if (cur == 0u) {
+            ++mine;
+            return true;
+        }
+        return (cur ^ fp) <= imask && dd_key<SMEM>(s_keys, g_keys, cur & imask) == k.m;
+        // (else another key took the slot: the next probe looks at the group again)
+    }
+    if (++k.probes > gmask) { // every group full: the wave is recounted
+        stuck = true;
+        return true;
+    }
+    return false;
+}
+
+// The keys of one bucket, each thread walking i = tid, tid + T, ... with two
+// keys in flight (a and b alternate probes, one probe per key per trip).
+// (A warp-sliced variant refilling lanes by ballot kept more lanes busy but
+// issued more instructions: C3 dedup wave 25.0 vs 23.0 ms.)
+template <int THREADS, bool SMEM>
+__device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t s_keys,
+                                          const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
+    uint32_t next = threadIdx.x;
+    DdKey a{0, next, 0}, b{0, next + THREADS, 0};
+    bool la = a.i < n, lb = b.i < n;
+    next += 2 * THREADS;
+    if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
+    if (lb) b.m = dd_key<SMEM>(s_keys, g_keys, b.i);
+    while (la || lb) {
+        if (la && dd_probe<SMEM>(a, sg, gmask, imask, s_keys, g_keys, mine, stuck)) {
+            a = DdKey{0, next, 0};
+            next += THREADS;
+            la = a.i < n;
+            if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
+        }
+        if (lb && dd_probe<SMEM>(b, sg, gmask, imask, s_keys, g_keys, mine, stuck)) {
+            b = DdKey{0, next, 0};
+            next += THREADS;
+            lb = b.i < n;
+            if (lb) b.m = dd_key<SMEM>(s_keys, g_keys, b.i);
+        }
+    }
+}
+
+// One CTA per bucket: the distinct count of its n mixed keys through a
+// shared-memory set of 32-bit slots.  A slot holds (fingerprint | index of
+// the key in the bucket); the keys themselves are staged in shared memory
+// by the bulk-copy engine (nbuf = 2: the next bucket's keys arrive while
+// this one is inserted), so a slot is 4 bytes (a group of 4 slots = one
+// LDS.128, the claim one 32-bit CAS) and a key is compared in full only on
+// a fingerprint match (a duplicate, or a 2^-(32-ib) accident).  ib = index
+// bits = max(16, bits(n - 1)); the fingerprint is the key's bits
+// [16 + ib, 48) (the bucket is its top bits, the group its low bits), never
+// 0, so 0 marks an empty slot.  Slots of a group fill in order and never
+// empty, so a key can only sit before its group's first empty slot: the set
+// is exact.  Buckets larger than a staging buffer read their keys from
+// global memory.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* off, uint64_t nbuckets,
+                                                          const unsigned long long* keys, const uint32_t* bucket_doc,
+                                                          unsigned long long* term_count, unsigned int* overflow,
+                                                          uint32_t slots, uint32_t kcap, uint32_t nbuf) {
+    extern __shared__ __align__(16) uint8_t dd_smem[];
+    uint4* s_grp = reinterpret_cast<uint4*>(dd_smem);                                          // slots / 4 groups
+    unsigned long long* s_buf = reinterpret_cast<unsigned long long*>(dd_smem + 4ull * slots); // nbuf x kcap keys
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_buf + static_cast<uint64_t>(nbuf) * kcap); // nbuf mbarriers
+    if (threadIdx.x == 0) {
+        for (uint32_t j = 0; j < nbuf; ++j) mbar_init(&s_bar[j], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t sg = static_cast<uint32_t>(__cvta_generic_to_shared(s_grp));
+    // keys [o0, o0 + n) staged from the 16-byte aligned key o0 & ~1 (keys is 256-byte aligned)
+    auto staged = [&](uint32_t o0, uint32_t n) { return n > 0 && ((n + (o0 & 1u) + 1u) & ~1u) <= kcap; };
+    auto prefetch = [&](uint64_t t, uint32_t b) {
+        const uint32_t o0 = off[t], n = off[t + 1] - o0;
+        if (staged(o0, n)) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // (after the generic reads of the buffer)
+            bulk_load(s_buf + b * kcap, keys + (o0 & ~1u), 8u * ((n + (o0 & 1u) + 1u) & ~1u), &s_bar[b]);
+        }
+    };
+    if (threadIdx.x == 0 && blockIdx.x < nbuckets) prefetch(blockIdx.x, 0);
+    uint32_t phase = 0; // parity bit per buffer
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < nbuckets; t += gridDim.x, ++it) {
+        const uint32_t b = nbuf > 1 ? (it & 1u) : 0u;
+        // (buffer b ^ 1 was released by the barrier that ended the previous bucket)
+        if (nbuf > 1 && threadIdx.x == 0 && t + gridDim.x < nbuckets) prefetch(t + gridDim.x, b ^ 1u);
+        const uint32_t o0 = off[t], n = off[t + 1] - o0;
+        if (n == 0) {
+            if (nbuf == 1 && threadIdx.x == 0 && t + gridDim.x < nbuckets) prefetch(t + gridDim.x, 0);
+            continue; // uniform over the CTA
+        }
+        const uint32_t ib = max(16, 32 - __clz(static_cast<int>(n - 1)));
+        uint32_t G = 64; // groups: load <= 2/3 where the launch's slots allow
+        while (G * 4 < n + n / 2 && G * 4 < slots) G <<= 1;
+        for (uint32_t j = threadIdx.x; j < G; j += THREADS) s_grp[j] = make_uint4(0u, 0u, 0u, 0u);
+        const bool st = staged(o0, n);
+        if (st) {
+            mbar_wait(&s_bar[b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+        }
+        __syncthreads(); // set cleared, keys staged
+        uint32_t mine = 0;
+        bool stuck = ib > 28; // (a bucket of > 2^28 keys: the wave is recounted)
+        if (!stuck) {
+            const uint32_t imask = (1u << ib) - 1u;
+            if (st)
+                dd_bucket<THREADS, true>(n, sg, G - 1u, imask,
+                                         static_cast<uint32_t>(__cvta_generic_to_shared(s_buf + b * kcap + (o0 & 1u))),
+                                         nullptr, mine, stuck);
+            else
+                dd_bucket<THREADS, false>(n, sg, G - 1u, imask, 0u, keys + o0, mine, stuck);
+        }
+        mine = __reduce_add_sync(0xffffffffu, mine);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&term_count[bucket_doc[t]], (unsigned long long)mine);
+        if (stuck) atomicOr(overflow, 1u);
+        __syncthreads(); // the set and buffer b are free again
+        if (nbuf == 1 && threadIdx.x == 0 && t + gridDim.x < nbuckets) prefetch(t + gridDim.x, 0);
     }
 }
 
@@ -1047,12 +1311,19 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         // bucket too skewed for its set is recounted by hashset_count
         auto partitioned_count = [&] {
             COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            // direct scatter + fingerprint dedup (default), or the two-level /
+            // single-level scatters with the 64-bit key sets (A/B knobs)
+            // COBS_PC_MODE: direct | two (two-level + fingerprint dedup) | legacy (two-level + 64-bit key sets)
+            const char* mode_env = std::getenv("COBS_PC_MODE");
+            const std::string mode = mode_env ? mode_env : "two";
+            const bool direct = mode == "direct";
+            const bool fp_dedup = mode != "legacy";
             const char* two_env = std::getenv("COBS_PC_TWO_LEVEL");
-            const bool two_level = sym_bits || (two_env ? two_env[0] != '0' : true); // symbol codes: two-level only
+            const bool two_level = !direct && (sym_bits || fp_dedup || (two_env ? two_env[0] != '0' : true)); // (single level: 2-bit codes only)
             uint64_t kmax = std::min<uint64_t>((free_b / 2) / (two_level ? 16 : 8), 0xffffffffull);
             if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
-            uint64_t target = kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
+            uint64_t target = fp_dedup ? kPcTargetDirect : kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
             if (const char* e = std::getenv("COBS_PC_TARGET")) target = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
             const uint64_t max_buckets = kmax / (target / 2) + 2 * n_docs + 1;
             // slots >= slot_mul x mean bucket keys + slack: 1x (A/B knob
@@ -1060,14 +1331,17 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             // (the dedup is bound by the shared-memory pipe), C3 count 1.81 -> 1.66 s
             double slot_mul = 1.0;
             if (const char* e = std::getenv("COBS_PC_SLOT_MUL")) slot_mul = std::atof(e);
+            // direct: keys per (chunk, bucket) run the chunk size aims at (A/B knob COBS_PC_RUNLEN)
+            uint64_t runlen = 256;
+            if (const char* e = std::getenv("COBS_PC_RUNLEN")) runlen = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
             // plan every wave up front (documents in order, keys <= kmax); the
             // waves then run back to back without a host round trip
-            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup; };
+            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup, ncc, kcap; };
             std::vector<PcWave> pw;
             std::vector<PcDoc> pd;
             std::vector<std::pair<uint64_t, uint64_t>> oversize; // documents beyond the key buffer
             for (uint64_t d0 = 0; d0 < n_docs;) {
-                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0, 0};
+                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0, 0, 0, 2};
                 uint64_t d1 = d0;
                 while (d1 < n_docs) {
                     const uint64_t W = doc_w[d1];
@@ -1077,12 +1351,24 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     const uint64_t mean = (W + nbk - 1) / nbk;
                     uint64_t slots = 256;
                     // (+ 6 sigma of a bucket's key count + slack: the fullest
-                    // bucket stays below ~90 % load)
-                    while (slots < slot_mul * 1.15 * mean + 6.0 * std::sqrt(static_cast<double>(mean)) + 256 &&
-                           slots < kPcMaxSlots)
-                        slots <<= 1;
+                    // bucket stays below ~90 % load; the 32-bit fingerprint
+                    // sets below 2/3)
+                    const double fullest = mean + 6.0 * std::sqrt(static_cast<double>(mean));
+                    if (fp_dedup) {
+                        while (slots < 1.5 * fullest + 256 && slots < kPcMaxSlotsFp) slots <<= 1;
+                        if (const char* e = std::getenv("COBS_PC_SLOTS_CAP")) // tests: sets too small -> recount
+                            slots = std::max<uint64_t>(256, std::min<uint64_t>(slots, std::strtoull(e, nullptr, 10)));
+                    }
+                    else
+                        while (slots < slot_mul * 1.15 * mean + 6.0 * std::sqrt(static_cast<double>(mean)) + 256 &&
+                               slots < kPcMaxSlots)
+                            slots <<= 1;
+                    // chunk size: direct runs of ~runlen keys per (chunk, bucket)
+                    uint64_t tpr = kPcRunsPerThread;
+                    if (direct) tpr = std::max<uint64_t>(tpr, (runlen * nbk + 256 * kBRun - 1) / (256 * kBRun));
                     if (d1 > d0 && (wv.keys + W > kmax || wv.nbuck + nbk > max_buckets)) break;
                     wv.slots = std::max(wv.slots, slots);
+                    wv.kcap = std::max<uint64_t>(wv.kcap, (static_cast<uint64_t>(fullest) + 4) & ~1ull);
                     PcDoc D{};
                     D.seg_lo = doc_segs[d1];
                     D.seg_hi = doc_segs[d1 + 1];
@@ -1094,11 +1380,15 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     D.shift = 64 - static_cast<uint32_t>(__builtin_ctzll(nbk));
                     D.doc = static_cast<uint32_t>(d1);
                     D.sb0 = static_cast<uint32_t>(wv.nsup);
+                    D.tpr = static_cast<uint32_t>(tpr);
+                    D.cc0 = wv.ncc;
                     pd.push_back(D);
+                    const uint64_t nch = (D.run_hi - D.run_lo + 256 * tpr - 1) / (256 * tpr);
                     wv.nsup += std::min<uint64_t>(nbk, kSup);
                     wv.keys += W;
                     wv.nbuck += nbk;
-                    wv.nchunk += (D.run_hi - D.run_lo + kPcRuns - 1) / kPcRuns;
+                    wv.nchunk += nch;
+                    if (direct) wv.ncc += nch * nbk;
                     ++d1;
                 }
                 wv.d1 = d1;
@@ -1110,17 +1400,19 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 }
                 d0 = d1;
             }
-            uint64_t max_keys = 1, max_nbuck = 1, max_nsup = 1;
+            uint64_t max_keys = 1, max_nbuck = 1, max_nsup = 1, max_ncc = 1;
             for (const PcWave& wv : pw) {
                 max_keys = std::max(max_keys, wv.keys);
                 max_nbuck = std::max(max_nbuck, wv.nbuck);
                 max_nsup = std::max(max_nsup, wv.nsup);
+                max_ncc = std::max(max_ncc, wv.ncc);
             }
             DevBuf d_keys, d_keys_a, d_sup_cur, d_sup_doc, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc;
-            d_keys.reserve(8 * max_keys);
+            d_keys.reserve(8 * max_keys + 16); // (+16: the dedup's 16-byte staged copies may read one key past the end)
             uint64_t max_nchunk = 1;
             for (const PcWave& wv : pw) max_nchunk = std::max(max_nchunk, wv.nchunk);
-            DevBuf d_chunk_sup;
+            DevBuf d_chunk_sup, d_chunk_cnt;
+            if (direct) d_chunk_cnt.reserve(4 * max_ncc);
             if (two_level) {
                 d_chunk_sup.reserve(4ull * kSup * max_nchunk);
                 d_keys_a.reserve(8 * max_keys);
@@ -1148,6 +1440,16 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             auto dedup = dthreads >= 1024 ? pc_dedup_kernel<1024> : dthreads >= 512 ? pc_dedup_kernel<512> : pc_dedup_kernel<256>;
             dthreads = dthreads >= 1024 ? 1024 : dthreads >= 512 ? 512 : 256;
             COBS_CUDA(cudaFuncSetAttribute(dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
+            auto dscat = sym_bits ? pc_scatter_direct_kernel<0, kSymBits>
+                         : q == 31 ? pc_scatter_direct_kernel<31> : pc_scatter_direct_kernel<0>;
+            COBS_CUDA(cudaFuncSetAttribute(dscat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
+            auto dedup_fp = dthreads >= 512 ? pc_dedup_fp_kernel<512> : pc_dedup_fp_kernel<256>;
+            const int fthreads = dthreads >= 512 ? 512 : 256;
+            // set + two key staging buffers + 2 mbarriers (a wave's kcap is capped so this fits)
+            uint32_t nbuf = 1; // key staging buffers (A/B knob COBS_PC_DD_NBUF = 1 / 2; 1: more CTAs per SM, faster)
+            if (const char* e = std::getenv("COBS_PC_DD_NBUF")) nbuf = std::atoi(e) == 1 ? 1u : 2u;
+            auto fp_smem = [&](uint64_t slots, uint64_t kcap) { return static_cast<size_t>(4 * slots + nbuf * (8 * kcap + 8)); };
+            COBS_CUDA(cudaFuncSetAttribute(dedup_fp, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
                 const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
@@ -1164,6 +1466,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pa.keys = d_keys.as<unsigned long long>();
                 pa.bad = flags;
                 pa.chunk_sup = two_level ? d_chunk_sup.as<uint32_t>() : nullptr;
+                pa.chunk_cnt = direct ? d_chunk_cnt.as<uint32_t>() : nullptr;
+                pa.mixed = fp_dedup ? 1 : 0;
+                pa.st_hint = std::getenv("COBS_PC_STHINT") ? std::atoi(std::getenv("COBS_PC_STHINT")) : 0;
                 pa.symtab = d_symtab.as<uint8_t>();
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
                 if (wv.nchunk) hist<<<grid, 256, 0, st>>>(pa);
@@ -1184,9 +1489,22 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                         pb, d_sup_cur.as<uint32_t>());
                     pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
                         d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
-                        d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
+                        d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>(), pa.mixed);
                 }
-                if (wv.nchunk) {
+                if (wv.nchunk && fp_dedup) {
+                    if (direct) {
+                        unsigned dgrid = grid; // (A/B knob COBS_PC_DGRID: CTAs per SM of the direct scatter)
+                        if (const char* e = std::getenv("COBS_PC_DGRID"))
+                            dgrid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148ull * std::atoi(e), wv.nchunk)));
+                        dscat<<<dgrid, 256, 2 * kPcHist * 4, st>>>(pa);
+                    }
+                    const uint64_t kcap = std::min<uint64_t>(wv.kcap, ((227 * 1024 - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
+                    dedup_fp<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), fthreads,
+                               fp_smem(wv.slots, kcap), st>>>(
+                        d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
+                        d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
+                        static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf);
+                } else if (wv.nchunk) {
                     if (!two_level) scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
                     dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dthreads, wv.slots * 8, st>>>(
                         d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
