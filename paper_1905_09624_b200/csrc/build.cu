@@ -3,10 +3,12 @@
 //   count pass  exact per-document distinct count -> term_count
 //               (termizer.cpp:103-129, termizer.hpp:25), windows rolled as
 //               2-bit codes (canonical = min(fwd, revcomp)):
-//               * partitioned (q <= 32, large corpora): codes split by a
-//                 bijective mix into per-document buckets (shared-memory
-//                 histograms, scan, scatter), each bucket deduplicated in a
-//                 shared-memory set -- pc_*_kernel;
+//               * partitioned (q <= 32, large corpora): codes mixed by a
+//                 bijection and split into per-document buckets (shared-
+//                 memory histograms, scan, a two-level scatter), each bucket
+//                 deduplicated in a shared-memory set of 32-bit
+//                 fingerprint|index slots over its keys staged by the bulk-
+//                 copy engine -- pc_*_kernel;
 //               * hash sets (any q, byte-path windows, small corpora):
 //                 per-document lock-free sets in L2-sized waves -- count_kernel.
 //   host        classic width / compact (term_count, name) sort, blocks of
@@ -286,20 +288,21 @@ __global__ void __launch_bounds__(256) count_kernel(WinArgs a, unsigned long lon
 
 // ---- partitioned distinct count (q <= 32: every counted window is a 2-bit
 // code).  Instead of one random L2/DRAM CAS per window into a per-document
-// hash set, each document's codes are split by the top bits of a bijective
-// mix into buckets of <= ~4,096 keys (chunk histograms in shared memory, one
-// global atomic per (chunk, bucket)), scattered into a key buffer, and every
-// bucket is deduplicated by one CTA in a shared-memory set.  Exact: a code
-// lands in exactly one bucket, and equal codes always in the same one.
+// hash set, each document's codes are mixed by a bijection (the keys) and
+// split by the keys' top bits into buckets of ~4,096 keys (chunk histograms
+// in shared memory, one global atomic per (chunk, bucket)), scattered into a
+// key buffer in two levels, and every bucket is deduplicated by one CTA in a
+// shared-memory set.  Exact: a code lands in exactly one bucket, and equal
+// codes always in the same one.
 #ifndef COBS_PC_RUNS
 #define COBS_PC_RUNS 16
 #endif
 constexpr uint32_t kPcRunsPerThread = COBS_PC_RUNS; // consecutive runs one thread rolls through
 constexpr uint32_t kPcRuns = 256 * kPcRunsPerThread; // runs (x kBRun windows) per chunk
 constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in shared memory
-constexpr uint32_t kPcMaxSlots = 16384; // largest dedup set (128 KB of shared memory)
 constexpr uint64_t kPcTarget = 4096;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
-constexpr uint64_t kPcTargetDirect = 4096; // the same for the fingerprint sets
+                                        // (A/B, fingerprint sets: 2,048 / 3,072 / 4,096 / 8,192 -> C3 count
+                                        // 1.78-1.91 / 1.49-1.52 / 1.41-1.50 / 1.74-1.78 s)
 constexpr uint32_t kPcMaxSlotsFp = 32768;  // largest fingerprint set (128 KB of shared memory)
                                         // (A/B with 1x-mean sets: 1,024 / 2,048 / 4,096 -> C3 count 1.81 / 1.65 / 1.61 s)
 
@@ -313,7 +316,6 @@ struct PcDoc {
     uint32_t doc;            // global document index
     uint32_t sb0;            // two-level scatter: first super-bucket (wave-relative prefix)
     uint32_t tpr;            // runs per thread in this document's chunks (a chunk = 256 x tpr runs)
-    uint64_t cc0;            // direct scatter: its (chunk, bucket) count matrix in chunk_cnt
 };
 
 struct PcArgs {
@@ -322,14 +324,10 @@ struct PcArgs {
     uint32_t ndocs;
     uint64_t nchunks;
     uint32_t* bucket_cnt;     // per bucket (histogram pass)
-    uint32_t* cursor;         // per bucket write cursor (= exclusive scan of bucket_cnt)
-    unsigned long long* keys; // code + 1, grouped by bucket
+    unsigned long long* keys; // mix_code(code) (a bijection), grouped by (super-)bucket
     unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
     uint32_t* chunk_sup;      // two-level: per (chunk, super-bucket) key counts [chunk][kSup], or null
-    uint32_t* chunk_cnt;      // direct: per (chunk, bucket) key counts at cc0 + local chunk x nbk, or null
     const uint8_t* symtab;    // SB > 0: byte -> symbol index (256 entries)
-    int mixed;                // keys are mix_code(code) (fingerprint dedup), else code + 1
-    int st_hint;              // direct scatter key stores: 0 plain, 1 L2 evict_last, 2 L2 evict_normal (A/B)
 };
 
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
@@ -402,10 +400,8 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
             s_bad = 0;
         }
         __syncthreads();
-        const PcDoc D = p.docs[s_doc];
-        const bool local = D.nbk <= kPcHist;
-        if (local)
-            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_hist[j] = 0;
+        const PcDoc D = p.docs[s_doc]; // (D.nbk <= kPcHist)
+        for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_hist[j] = 0;
         __syncthreads();
         uint64_t r0, r1;
         pc_chunk_runs(D, c, r0, r1);
@@ -415,23 +411,13 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
                 bad += p.a.canonical ? 0u : 1u;
                 return;
             }
-            const uint32_t b = pc_bucket(code, D.shift);
-            if (local)
-                atomicAdd(&s_hist[b], 1u);
-            else
-                atomicAdd(&p.bucket_cnt[D.bucket0 + b], 1u);
+            atomicAdd(&s_hist[pc_bucket(code, D.shift)], 1u);
         }, s_sym);
         if (bad) atomicAdd(&s_bad, (unsigned long long)bad);
         __syncthreads();
-        if (local) {
-            uint32_t* cc = p.chunk_cnt ? p.chunk_cnt + D.cc0 + (c - D.chunk0) * D.nbk : nullptr;
-            for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) {
-                const uint32_t h = s_hist[j];
-                if (h) atomicAdd(&p.bucket_cnt[D.bucket0 + j], h);
-                if (cc) cc[j] = h; // the direct scatter's reservation sizes
-            }
-        }
-        if (local && p.chunk_sup) { // the two-level scatter's per-chunk super-bucket counts
+        for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x)
+            if (s_hist[j]) atomicAdd(&p.bucket_cnt[D.bucket0 + j], s_hist[j]);
+        { // the super-bucket scatter's per-chunk reservation sizes
             const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
             if (threadIdx.x < nsb) {
                 uint32_t sum = 0;
@@ -440,59 +426,6 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
             }
         }
         if (threadIdx.x == 0 && s_bad) atomicAdd(p.bad, s_bad);
-    }
-}
-
-template <int QC>
-__global__ void __launch_bounds__(256) pc_scatter_kernel(PcArgs p) {
-    extern __shared__ uint32_t pc_smem[];
-    uint32_t* s_cnt = pc_smem;            // kPcHist
-    uint32_t* s_base = pc_smem + kPcHist; // kPcHist
-    __shared__ uint32_t s_doc;
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
-        __syncthreads();
-        const PcDoc D = p.docs[s_doc];
-        uint64_t r0, r1;
-        pc_chunk_runs(D, c, r0, r1);
-        if (D.nbk > kPcHist) { // very large document: one global cursor atomic per key
-            pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
-                if (!dna) return;
-                const uint32_t pos = atomicAdd(&p.cursor[D.bucket0 + pc_bucket(code, D.shift)], 1u);
-                p.keys[pos] = code + 1ull;
-            });
-            continue;
-        }
-        for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) s_cnt[j] = 0;
-        __syncthreads();
-        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
-            if (dna) atomicAdd(&s_cnt[pc_bucket(code, D.shift)], 1u);
-        });
-        __syncthreads();
-        for (uint32_t j0 = threadIdx.x; j0 < D.nbk; j0 += 4 * blockDim.x) { // 4 reservations in flight
-            uint32_t n[4], base[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * blockDim.x;
-                n[u] = j < D.nbk ? s_cnt[j] : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (n[u]) base[u] = atomicAdd(&p.cursor[D.bucket0 + j0 + u * blockDim.x], n[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * blockDim.x;
-                if (n[u]) s_base[j] = base[u];
-                if (j < D.nbk) s_cnt[j] = 0;
-            }
-        }
-        __syncthreads();
-        pc_windows<QC>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
-            if (!dna) return;
-            const uint32_t b = pc_bucket(code, D.shift);
-            p.keys[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = code + 1ull;
-        });
     }
 }
 
@@ -530,16 +463,8 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
         uint64_t r0, r1;
         pc_chunk_runs(D, c, r0, r1);
         const uint32_t sbs = pc_super_shift(D), nsb = D.nbk >> sbs;
-        const bool counted = p.chunk_sup && D.nbk <= kPcHist; // the histogram pass left the counts
-        if (threadIdx.x < kSup) s_cnt[threadIdx.x] = 0;
-        __syncthreads();
-        if (!counted)
-            pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
-                if (dna) atomicAdd(&s_cnt[pc_bucket(code, D.shift) >> sbs], 1u);
-            }, s_sym);
-        __syncthreads();
-        if (threadIdx.x < nsb) {
-            const uint32_t n = counted ? p.chunk_sup[c * kSup + threadIdx.x] : s_cnt[threadIdx.x];
+        if (threadIdx.x < nsb) { // (the histogram pass left the chunk's counts)
+            const uint32_t n = p.chunk_sup[c * kSup + threadIdx.x];
             if (n) s_base[threadIdx.x] = atomicAdd(&sup_cursor[D.sb0 + threadIdx.x], n);
             s_cnt[threadIdx.x] = 0;
         }
@@ -548,7 +473,7 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
             if (!dna) return;
             const uint64_t m = mix_code(code);
             const uint32_t sb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(m >> D.shift)) >> sbs;
-            p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = p.mixed ? m : code + 1ull;
+            p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = m;
         }, s_sym);
     }
 }
@@ -562,7 +487,7 @@ constexpr uint32_t kFinPer = kFinTile / 256; // keys per thread per tile
 __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs, const uint32_t* sup_doc,
                                                                uint64_t nsup, const uint32_t* off,
                                                                const unsigned long long* keys_a,
-                                                               unsigned long long* keys_b, int mixed) {
+                                                               unsigned long long* keys_b) {
     constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
     __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB];
     __shared__ unsigned long long s_sorted[kFinTile];
@@ -589,8 +514,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
             for (uint32_t u = 0; u < kFinPer; ++u) {
                 lr[u] = 0;
                 if (threadIdx.x + u * blockDim.x < n) {
-                    const uint32_t lb = (mixed ? (D.shift >= 64 ? 0u : static_cast<uint32_t>(kv[u] >> D.shift))
-                                               : pc_bucket(kv[u] - 1ull, D.shift)) & (bps - 1u);
+                    const uint32_t lb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(kv[u] >> D.shift)) & (bps - 1u);
                     lr[u] = lb | (atomicAdd(&s_cnt[lb], 1u) << 8);
                 }
             }
@@ -627,68 +551,6 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
         }
     }
 }
-
-// ---- direct scatter + fingerprint dedup (one key round trip) ----------
-//
-// The histogram pass leaves every (chunk, bucket) count; a chunk reserves
-// each bucket's run with one cursor atomic and writes its keys there.  Chunks
-// are sized per document (256 x D.tpr runs) so a (chunk, bucket) run is a
-// few hundred keys -- whole DRAM sectors -- even at thousands of buckets.
-// Keys are stored mixed (mix_code is a bijection, so distinctness is kept):
-// the bucket is the key's top bits and the dedup needs no re-mix.
-template <int QC, int SB = 0>
-__global__ void __launch_bounds__(256) pc_scatter_direct_kernel(PcArgs p) {
-    extern __shared__ uint32_t pc_smem[];
-    uint32_t* s_cnt = pc_smem;            // <= kPcHist
-    uint32_t* s_base = pc_smem + kPcHist; // <= kPcHist
-    __shared__ uint32_t s_doc;
-    __shared__ uint8_t s_sym[256];
-    if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
-        __syncthreads();
-        const PcDoc D = p.docs[s_doc];
-        uint64_t r0, r1;
-        pc_chunk_runs(D, c, r0, r1);
-        const uint32_t* cc = p.chunk_cnt + D.cc0 + (c - D.chunk0) * D.nbk;
-        for (uint32_t j0 = threadIdx.x; j0 < D.nbk; j0 += 4 * blockDim.x) { // 4 reservations in flight
-            uint32_t n[4], base[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * blockDim.x;
-                n[u] = j < D.nbk ? cc[j] : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (n[u]) base[u] = atomicAdd(&p.cursor[D.bucket0 + j0 + u * blockDim.x], n[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * blockDim.x;
-                if (n[u]) s_base[j] = base[u];
-                if (j < D.nbk) s_cnt[j] = 0;
-            }
-        }
-        __syncthreads();
-        pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
-            if (!dna) return;
-            const uint64_t m = mix_code(code);
-            const uint32_t b = D.shift >= 64 ? 0u : static_cast<uint32_t>(m >> D.shift);
-            unsigned long long* dst = p.keys + s_base[b] + atomicAdd(&s_cnt[b], 1u);
-            if (p.st_hint == 0) {
-                *dst = m;
-            } else {
-                uint64_t pol;
-                if (p.st_hint == 1)
-                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-                else
-                    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-                asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(dst), "l"(m), "l"(pol) : "memory");
-            }
-        }, s_sym);
-    }
-}
-
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
@@ -729,9 +591,10 @@ struct DdKey {
     uint32_t i, probes;
 };
 template <bool SMEM>
-__device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t s_keys,
+__device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
+                                         uint32_t s_keys,
                                          const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
-    uint32_t fp = static_cast<uint32_t>(k.m >> 16) & ~imask;
+    uint32_t fp = static_cast<uint32_t>(k.m >> 16) & fmask; // (fmask = ~imask; tests narrow it)
     fp = fp ? fp : imask + 1u;
     const uint32_t gaddr = sg + 16u * ((static_cast<uint32_t>(k.m) + k.probes) & gmask);
     uint4 v;
@@ -767,7 +630,8 @@ __device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, 
 // (A warp-sliced variant refilling lanes by ballot kept more lanes busy but
 // issued more instructions: C3 dedup wave 25.0 vs 23.0 ms.)
 template <int THREADS, bool SMEM>
-__device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t s_keys,
+__device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
+                                          uint32_t s_keys,
                                           const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
     uint32_t next = threadIdx.x;
     DdKey a{0, next, 0}, b{0, next + THREADS, 0};
@@ -776,13 +640,13 @@ __device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmas
     if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
     if (lb) b.m = dd_key<SMEM>(s_keys, g_keys, b.i);
     while (la || lb) {
-        if (la && dd_probe<SMEM>(a, sg, gmask, imask, s_keys, g_keys, mine, stuck)) {
+        if (la && dd_probe<SMEM>(a, sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
             a = DdKey{0, next, 0};
             next += THREADS;
             la = a.i < n;
             if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
         }
-        if (lb && dd_probe<SMEM>(b, sg, gmask, imask, s_keys, g_keys, mine, stuck)) {
+        if (lb && dd_probe<SMEM>(b, sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
             b = DdKey{0, next, 0};
             next += THREADS;
             lb = b.i < n;
@@ -808,7 +672,8 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* off, uint64_t nbuckets,
                                                           const unsigned long long* keys, const uint32_t* bucket_doc,
                                                           unsigned long long* term_count, unsigned int* overflow,
-                                                          uint32_t slots, uint32_t kcap, uint32_t nbuf) {
+                                                          uint32_t slots, uint32_t kcap, uint32_t nbuf,
+                                                          uint32_t fp_test_mask) {
     extern __shared__ __align__(16) uint8_t dd_smem[];
     uint4* s_grp = reinterpret_cast<uint4*>(dd_smem);                                          // slots / 4 groups
     unsigned long long* s_buf = reinterpret_cast<unsigned long long*>(dd_smem + 4ull * slots); // nbuf x kcap keys
@@ -855,11 +720,11 @@ __global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* of
         if (!stuck) {
             const uint32_t imask = (1u << ib) - 1u;
             if (st)
-                dd_bucket<THREADS, true>(n, sg, G - 1u, imask,
+                dd_bucket<THREADS, true>(n, sg, G - 1u, imask, ~imask & fp_test_mask,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(s_buf + b * kcap + (o0 & 1u))),
                                          nullptr, mine, stuck);
             else
-                dd_bucket<THREADS, false>(n, sg, G - 1u, imask, 0u, keys + o0, mine, stuck);
+                dd_bucket<THREADS, false>(n, sg, G - 1u, imask, ~imask & fp_test_mask, 0u, keys + o0, mine, stuck);
         }
         mine = __reduce_add_sync(0xffffffffu, mine);
         if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&term_count[bucket_doc[t]], (unsigned long long)mine);
@@ -923,74 +788,6 @@ __global__ void pc_bdoc_kernel(const PcDoc* docs, uint32_t ndocs, uint32_t* buck
     for (uint32_t i = blockIdx.x; i < ndocs; i += gridDim.x) {
         const PcDoc D = docs[i];
         for (uint32_t j = threadIdx.x; j < D.nbk; j += blockDim.x) bucket_doc[D.bucket0 + j] = D.doc;
-    }
-}
-
-// one CTA per bucket: distinct keys through a shared-memory set sized to the
-// bucket; the count goes to the bucket's document
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) pc_dedup_kernel(const uint32_t* off, uint64_t nbuckets,
-                                                       const unsigned long long* keys, const uint32_t* bucket_doc,
-                                                       unsigned long long* term_count, unsigned int* overflow,
-                                                       uint32_t slots) {
-    extern __shared__ unsigned long long s_tab[]; // `slots` (sized per wave: 2x its largest mean bucket)
-    for (uint64_t t = blockIdx.x; t < nbuckets; t += gridDim.x) {
-        const uint32_t o0 = off[t], o1 = off[t + 1];
-        if (o0 == o1) continue; // uniform over the CTA
-        uint32_t S = 64, S_log2 = 6; // (>= 16 groups of 4)
-        while (S < 2 * (o1 - o0) && S < slots) {
-            S <<= 1;
-            ++S_log2;
-        }
-        __syncthreads(); // the previous bucket's inserts are done
-        for (uint32_t j = threadIdx.x; j < S / 2; j += blockDim.x)
-            reinterpret_cast<ulonglong2*>(s_tab)[j] = make_ulonglong2(0ull, 0ull);
-        __syncthreads();
-        uint32_t mine = 0;
-        bool stuck = false;
-        // Bucketised set: S/4 groups of 4 slots (32 bytes, two LDS.128); a key
-        // looks in its group and claims the group's first empty slot with one
-        // CAS (re-read on a lost race), or moves to the next group when all
-        // four hold other keys.  Keys of a bucket are codes spread by the
-        // bucket's mix, so a 32-bit multiplicative hash suffices for the group.
-        const uint32_t gmask = S / 4 - 1;
-        auto insert = [&](unsigned long long key) {
-            uint32_t g = ((static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * 0x9E3779B1u) >> (34 - S_log2);
-            for (uint32_t probes = 0; probes <= gmask;) {
-                unsigned long long* grp = s_tab + 4 * g;
-                const ulonglong2 lo = *reinterpret_cast<const ulonglong2*>(grp);
-                const ulonglong2 hi = *reinterpret_cast<const ulonglong2*>(grp + 2);
-                if (lo.x == key || lo.y == key || hi.x == key || hi.y == key) return;
-                const int e = lo.x == 0ull ? 0 : lo.y == 0ull ? 1 : hi.x == 0ull ? 2 : hi.y == 0ull ? 3 : 4;
-                if (e == 4) { // all four hold other keys
-                    g = (g + 1) & gmask;
-                    ++probes;
-                    continue;
-                }
-                const unsigned long long cur = atomicCAS(grp + e, 0ull, key);
-                if (cur == 0ull) {
-                    ++mine;
-                    return;
-                }
-                if (cur == key) return; // (else another key took the slot: look again)
-            }
-            stuck = true; // every group full: the wave is recounted
-        };
-        // 8 independent key loads in flight per thread, then the inserts
-        for (uint32_t i0 = o0 + threadIdx.x; i0 < o1; i0 += 8 * blockDim.x) {
-            unsigned long long kv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t i = i0 + u * blockDim.x;
-                kv[u] = i < o1 ? __ldcs(keys + i) : 0ull;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (kv[u]) insert(kv[u]);
-        }
-        mine = __reduce_add_sync(0xffffffffu, mine);
-        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&term_count[bucket_doc[t]], (unsigned long long)mine);
-        if (stuck) atomicOr(overflow, 1u);
     }
 }
 
@@ -1311,61 +1108,34 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         // bucket too skewed for its set is recounted by hashset_count
         auto partitioned_count = [&] {
             COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            // direct scatter + fingerprint dedup (default), or the two-level /
-            // single-level scatters with the 64-bit key sets (A/B knobs)
-            // COBS_PC_MODE: direct | two (two-level + fingerprint dedup) | legacy (two-level + 64-bit key sets)
-            const char* mode_env = std::getenv("COBS_PC_MODE");
-            const std::string mode = mode_env ? mode_env : "two";
-            const bool direct = mode == "direct";
-            const bool fp_dedup = mode != "legacy";
-            const char* two_env = std::getenv("COBS_PC_TWO_LEVEL");
-            const bool two_level = !direct && (sym_bits || fp_dedup || (two_env ? two_env[0] != '0' : true)); // (single level: 2-bit codes only)
-            uint64_t kmax = std::min<uint64_t>((free_b / 2) / (two_level ? 16 : 8), 0xffffffffull);
+            // two key buffers (super-bucket scatter, final placement), 16 bytes per window
+            uint64_t kmax = std::min<uint64_t>((free_b / 2) / 16, 0xffffffffull);
             if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
-            uint64_t target = fp_dedup ? kPcTargetDirect : kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
+            uint64_t target = kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
             if (const char* e = std::getenv("COBS_PC_TARGET")) target = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
             const uint64_t max_buckets = kmax / (target / 2) + 2 * n_docs + 1;
-            // slots >= slot_mul x mean bucket keys + slack: 1x (A/B knob
-            // COBS_PC_SLOT_MUL) -- the smaller sets let more CTAs share an SM
-            // (the dedup is bound by the shared-memory pipe), C3 count 1.81 -> 1.66 s
-            double slot_mul = 1.0;
-            if (const char* e = std::getenv("COBS_PC_SLOT_MUL")) slot_mul = std::atof(e);
-            // direct: keys per (chunk, bucket) run the chunk size aims at (A/B knob COBS_PC_RUNLEN)
-            uint64_t runlen = 256;
-            if (const char* e = std::getenv("COBS_PC_RUNLEN")) runlen = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
             // plan every wave up front (documents in order, keys <= kmax); the
             // waves then run back to back without a host round trip
-            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup, ncc, kcap; };
+            struct PcWave { uint64_t d0, d1, doc0, nbuck, nchunk, slots, keys, nsup, kcap; };
             std::vector<PcWave> pw;
             std::vector<PcDoc> pd;
             std::vector<std::pair<uint64_t, uint64_t>> oversize; // documents beyond the key buffer
             for (uint64_t d0 = 0; d0 < n_docs;) {
-                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0, 0, 0, 2};
+                PcWave wv{d0, d0, pd.size(), 0, 0, 256, 0, 0, 2};
                 uint64_t d1 = d0;
                 while (d1 < n_docs) {
                     const uint64_t W = doc_w[d1];
                     uint64_t nbk = 1;
                     while (nbk * target < W && nbk < kPcHist) nbk <<= 1;
-                    // the set must hold a bucket's distinct keys: mean W / nbk, plus slack
+                    // the set must hold a bucket's distinct keys: mean W / nbk
+                    // + 6 sigma of a bucket's key count, at load <= 2/3
                     const uint64_t mean = (W + nbk - 1) / nbk;
-                    uint64_t slots = 256;
-                    // (+ 6 sigma of a bucket's key count + slack: the fullest
-                    // bucket stays below ~90 % load; the 32-bit fingerprint
-                    // sets below 2/3)
                     const double fullest = mean + 6.0 * std::sqrt(static_cast<double>(mean));
-                    if (fp_dedup) {
-                        while (slots < 1.5 * fullest + 256 && slots < kPcMaxSlotsFp) slots <<= 1;
-                        if (const char* e = std::getenv("COBS_PC_SLOTS_CAP")) // tests: sets too small -> recount
-                            slots = std::max<uint64_t>(256, std::min<uint64_t>(slots, std::strtoull(e, nullptr, 10)));
-                    }
-                    else
-                        while (slots < slot_mul * 1.15 * mean + 6.0 * std::sqrt(static_cast<double>(mean)) + 256 &&
-                               slots < kPcMaxSlots)
-                            slots <<= 1;
-                    // chunk size: direct runs of ~runlen keys per (chunk, bucket)
-                    uint64_t tpr = kPcRunsPerThread;
-                    if (direct) tpr = std::max<uint64_t>(tpr, (runlen * nbk + 256 * kBRun - 1) / (256 * kBRun));
+                    uint64_t slots = 256;
+                    while (slots < 1.5 * fullest + 256 && slots < kPcMaxSlotsFp) slots <<= 1;
+                    if (const char* e = std::getenv("COBS_PC_SLOTS_CAP")) // tests: sets too small -> recount
+                        slots = std::max<uint64_t>(256, std::min<uint64_t>(slots, std::strtoull(e, nullptr, 10)));
                     if (d1 > d0 && (wv.keys + W > kmax || wv.nbuck + nbk > max_buckets)) break;
                     wv.slots = std::max(wv.slots, slots);
                     wv.kcap = std::max<uint64_t>(wv.kcap, (static_cast<uint64_t>(fullest) + 4) & ~1ull);
@@ -1380,15 +1150,12 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     D.shift = 64 - static_cast<uint32_t>(__builtin_ctzll(nbk));
                     D.doc = static_cast<uint32_t>(d1);
                     D.sb0 = static_cast<uint32_t>(wv.nsup);
-                    D.tpr = static_cast<uint32_t>(tpr);
-                    D.cc0 = wv.ncc;
+                    D.tpr = kPcRunsPerThread;
                     pd.push_back(D);
-                    const uint64_t nch = (D.run_hi - D.run_lo + 256 * tpr - 1) / (256 * tpr);
                     wv.nsup += std::min<uint64_t>(nbk, kSup);
                     wv.keys += W;
                     wv.nbuck += nbk;
-                    wv.nchunk += nch;
-                    if (direct) wv.ncc += nch * nbk;
+                    wv.nchunk += (D.run_hi - D.run_lo + kPcRuns - 1) / kPcRuns;
                     ++d1;
                 }
                 wv.d1 = d1;
@@ -1400,25 +1167,19 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 }
                 d0 = d1;
             }
-            uint64_t max_keys = 1, max_nbuck = 1, max_nsup = 1, max_ncc = 1;
+            uint64_t max_keys = 1, max_nbuck = 1, max_nsup = 1, max_nchunk = 1;
             for (const PcWave& wv : pw) {
                 max_keys = std::max(max_keys, wv.keys);
                 max_nbuck = std::max(max_nbuck, wv.nbuck);
                 max_nsup = std::max(max_nsup, wv.nsup);
-                max_ncc = std::max(max_ncc, wv.ncc);
+                max_nchunk = std::max(max_nchunk, wv.nchunk);
             }
-            DevBuf d_keys, d_keys_a, d_sup_cur, d_sup_doc, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc;
+            DevBuf d_keys, d_keys_a, d_sup_cur, d_sup_doc, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc, d_chunk_sup;
             d_keys.reserve(8 * max_keys + 16); // (+16: the dedup's 16-byte staged copies may read one key past the end)
-            uint64_t max_nchunk = 1;
-            for (const PcWave& wv : pw) max_nchunk = std::max(max_nchunk, wv.nchunk);
-            DevBuf d_chunk_sup, d_chunk_cnt;
-            if (direct) d_chunk_cnt.reserve(4 * max_ncc);
-            if (two_level) {
-                d_chunk_sup.reserve(4ull * kSup * max_nchunk);
-                d_keys_a.reserve(8 * max_keys);
-                d_sup_cur.reserve(4 * max_nsup);
-                d_sup_doc.reserve(4 * max_nsup);
-            }
+            d_keys_a.reserve(8 * max_keys);
+            d_chunk_sup.reserve(4ull * kSup * max_nchunk);
+            d_sup_cur.reserve(4 * max_nsup);
+            d_sup_doc.reserve(4 * max_nsup);
             d_flags.reserve(16 * std::max<size_t>(pw.size(), 1));
             d_cnt.reserve(4 * (max_nbuck + 1));
             d_off.reserve(4 * (max_nbuck + 1));
@@ -1432,24 +1193,21 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
             COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
             auto hist = sym_bits ? pc_hist_kernel<0, kSymBits> : q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
-            auto scat = q == 31 ? pc_scatter_kernel<31> : pc_scatter_kernel<0>;
-            COBS_CUDA(cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
-            // dedup CTA size (A/B knob COBS_PC_DEDUP_THREADS = 256 / 512 / 1024)
-            int dthreads = 256;
-            if (const char* e = std::getenv("COBS_PC_DEDUP_THREADS")) dthreads = std::atoi(e);
-            auto dedup = dthreads >= 1024 ? pc_dedup_kernel<1024> : dthreads >= 512 ? pc_dedup_kernel<512> : pc_dedup_kernel<256>;
-            dthreads = dthreads >= 1024 ? 1024 : dthreads >= 512 ? 512 : 256;
-            COBS_CUDA(cudaFuncSetAttribute(dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcMaxSlots * 8));
-            auto dscat = sym_bits ? pc_scatter_direct_kernel<0, kSymBits>
-                         : q == 31 ? pc_scatter_direct_kernel<31> : pc_scatter_direct_kernel<0>;
-            COBS_CUDA(cudaFuncSetAttribute(dscat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kPcHist * 4));
-            auto dedup_fp = dthreads >= 512 ? pc_dedup_fp_kernel<512> : pc_dedup_fp_kernel<256>;
-            const int fthreads = dthreads >= 512 ? 512 : 256;
-            // set + two key staging buffers + 2 mbarriers (a wave's kcap is capped so this fits)
+            auto scat = sym_bits ? pc_scatter_super_kernel<0, kSymBits>
+                        : q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>;
+            // dedup CTA size (A/B knob COBS_PC_DEDUP_THREADS = 256 / 512: within noise)
+            const char* dt_env = std::getenv("COBS_PC_DEDUP_THREADS");
+            const bool dd512 = dt_env && std::atoi(dt_env) >= 512;
+            auto dedup = dd512 ? pc_dedup_fp_kernel<512> : pc_dedup_fp_kernel<256>;
+            // set + key staging buffer(s) + mbarrier(s) (a wave's kcap is capped so this fits)
             uint32_t nbuf = 1; // key staging buffers (A/B knob COBS_PC_DD_NBUF = 1 / 2; 1: more CTAs per SM, faster)
             if (const char* e = std::getenv("COBS_PC_DD_NBUF")) nbuf = std::atoi(e) == 1 ? 1u : 2u;
-            auto fp_smem = [&](uint64_t slots, uint64_t kcap) { return static_cast<size_t>(4 * slots + nbuf * (8 * kcap + 8)); };
-            COBS_CUDA(cudaFuncSetAttribute(dedup_fp, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            auto dd_smem = [&](uint64_t slots, uint64_t kcap) { return static_cast<size_t>(4 * slots + nbuf * (8 * kcap + 8)); };
+            COBS_CUDA(cudaFuncSetAttribute(dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            // tests narrow the fingerprints to force accidental matches (COBS_PC_FP_MASK, e.g. 0x30000)
+            const uint32_t fp_test_mask = std::getenv("COBS_PC_FP_MASK")
+                                              ? static_cast<uint32_t>(std::strtoul(std::getenv("COBS_PC_FP_MASK"), nullptr, 0))
+                                              : 0xffffffffu;
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
                 const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
@@ -1463,54 +1221,29 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pa.ndocs = nd;
                 pa.nchunks = wv.nchunk;
                 pa.bucket_cnt = d_cnt.as<uint32_t>();
-                pa.keys = d_keys.as<unsigned long long>();
+                pa.keys = d_keys_a.as<unsigned long long>();
                 pa.bad = flags;
-                pa.chunk_sup = two_level ? d_chunk_sup.as<uint32_t>() : nullptr;
-                pa.chunk_cnt = direct ? d_chunk_cnt.as<uint32_t>() : nullptr;
-                pa.mixed = fp_dedup ? 1 : 0;
-                pa.st_hint = std::getenv("COBS_PC_STHINT") ? std::atoi(std::getenv("COBS_PC_STHINT")) : 0;
+                pa.chunk_sup = d_chunk_sup.as<uint32_t>();
                 pa.symtab = d_symtab.as<uint8_t>();
+                if (!wv.nchunk) continue;
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
-                if (wv.nchunk) hist<<<grid, 256, 0, st>>>(pa);
+                hist<<<grid, 256, 0, st>>>(pa);
                 size_t tb = d_tmp.bytes;
                 COBS_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.ptr, tb, d_cnt.as<uint32_t>(), d_off.as<uint32_t>(),
                                                         static_cast<int>(wv.nbuck + 1), st));
-                // the scan is both the dedup's bucket offsets and (a copy) the scatter cursors
-                COBS_CUDA(cudaMemcpyAsync(d_cnt.ptr, d_off.ptr, 4 * (wv.nbuck + 1), cudaMemcpyDeviceToDevice, st));
-                pa.cursor = d_cnt.as<uint32_t>();
-                if (wv.nchunk && two_level) {
-                    pc_super_init_kernel<<<std::min<uint32_t>(nd, 148 * 8), kSup, 0, st>>>(
-                        d_docs.as<PcDoc>() + wv.doc0, nd, d_off.as<uint32_t>(), d_sup_cur.as<uint32_t>(),
-                        d_sup_doc.as<uint32_t>());
-                    PcArgs pb = pa;
-                    pb.keys = d_keys_a.as<unsigned long long>();
-                    (sym_bits ? pc_scatter_super_kernel<0, kSymBits>
-                              : q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>)<<<grid, 256, 0, st>>>(
-                        pb, d_sup_cur.as<uint32_t>());
-                    pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
-                        d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
-                        d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>(), pa.mixed);
-                }
-                if (wv.nchunk && fp_dedup) {
-                    if (direct) {
-                        unsigned dgrid = grid; // (A/B knob COBS_PC_DGRID: CTAs per SM of the direct scatter)
-                        if (const char* e = std::getenv("COBS_PC_DGRID"))
-                            dgrid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148ull * std::atoi(e), wv.nchunk)));
-                        dscat<<<dgrid, 256, 2 * kPcHist * 4, st>>>(pa);
-                    }
-                    const uint64_t kcap = std::min<uint64_t>(wv.kcap, ((227 * 1024 - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
-                    dedup_fp<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), fthreads,
-                               fp_smem(wv.slots, kcap), st>>>(
-                        d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
-                        d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
-                        static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf);
-                } else if (wv.nchunk) {
-                    if (!two_level) scat<<<grid, 256, 2 * kPcHist * 4, st>>>(pa);
-                    dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dthreads, wv.slots * 8, st>>>(
-                        d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
-                        d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
-                        static_cast<uint32_t>(wv.slots));
-                }
+                pc_super_init_kernel<<<std::min<uint32_t>(nd, 148 * 8), kSup, 0, st>>>(
+                    d_docs.as<PcDoc>() + wv.doc0, nd, d_off.as<uint32_t>(), d_sup_cur.as<uint32_t>(),
+                    d_sup_doc.as<uint32_t>());
+                scat<<<grid, 256, 0, st>>>(pa, d_sup_cur.as<uint32_t>());
+                pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
+                    d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
+                    d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
+                const uint64_t kcap = std::min<uint64_t>(wv.kcap, ((227 * 1024 - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
+                dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dd512 ? 512 : 256,
+                        dd_smem(wv.slots, kcap), st>>>(
+                    d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
+                    d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
+                    static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf, fp_test_mask);
                 COBS_CUDA(cudaGetLastError());
             }
             g_timing.count_waves = static_cast<uint32_t>(pw.size());

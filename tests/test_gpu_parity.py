@@ -480,21 +480,15 @@ def test_count_partitioned_vs_hashset(gpu):
             want = O.build_image(corpus, q=q, canonical=canonical, block_size=16, kind=1)
             assert _build_env(corpus, params, cb.KIND_COMPACT) == want, (q, canonical)
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_COUNT_PARTITION=0) == want
-            # fingerprint sets capped too small (every wave recounted)
+            # fingerprint sets capped too small (every wave recounted), and
+            # small buckets (many per document, keys staged per bucket)
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_SLOTS_CAP=256) == want
-            # direct scatter: one chunk per document / minimal chunks
-            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_MODE="direct", COBS_PC_RUNLEN=10**6) == want
-            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_MODE="direct", COBS_PC_RUNLEN=1,
-                              COBS_PC_TARGET=512) == want
-            # the two-level scatter with 64-bit key sets
-            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_MODE="legacy") == want
-            # the single-level key scatter (COBS_PC_TWO_LEVEL=0) counts the same
-            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_COUNT_PARTITION=1,
-                              COBS_PC_TWO_LEVEL=0, COBS_PC_MODE="legacy") == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_TARGET=512) == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_NBUF=2, COBS_PC_DEDUP_THREADS=512) == want
+            # 2-bit fingerprints: most probes meet accidental matches and compare whole keys
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_FP_MASK=0x30000) == want
             # waves of <= 150,000 keys: many waves, and "big"/"polyA" exceed one
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_WAVE_KEYS=150000) == want
-            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_WAVE_KEYS=150000,
-                              COBS_PC_TWO_LEVEL=0, COBS_PC_MODE="legacy") == want
             # without the up-front byte scan: the wave holding "withN" is
             # recounted by the hash sets after the partitioned pass flags it
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_NO_SCAN=1,
@@ -524,8 +518,8 @@ def test_count_partitioned_symbol_codes(gpu):
 
 
 def test_count_partitioned_huge_document(gpu):
-    """A document with more buckets than a chunk histogram holds in shared
-    memory (> 8,192 x 4,096 windows): global-cursor scatter path."""
+    """A document with more buckets than a chunk histogram holds (> 8,192 x
+    4,096 windows): buckets above the target size (larger sets)."""
     rng = np.random.default_rng(9)
     big = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, 36_000_000)].tobytes()
     docs = [(b"huge", [big]), (b"small", [big[:5000]]), (b"mid", [big[1000:800000]])]
@@ -533,7 +527,6 @@ def test_count_partitioned_huge_document(gpu):
     a = _build_env(docs, params, cb.KIND_CLASSIC)
     b = _build_env(docs, params, cb.KIND_CLASSIC, COBS_COUNT_PARTITION=0)
     assert a == b
-    assert _build_env(docs, params, cb.KIND_CLASSIC, COBS_PC_TWO_LEVEL=0, COBS_PC_MODE="legacy") == a
     view = cb.open_image(a, 0)
     got = dict(view.doc(0, i) for i in range(view.doc_count(0)))
     view.close()
