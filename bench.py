@@ -586,18 +586,21 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
                           "algo_gbs": (int(lengths.sum()) + index_bytes) / ((c + f) / 1e3) / 1e9}}
     # Rooflines of the two passes against the measured HBM copy peak.  Neither
     # is HBM-bound: the count's design traffic (corpus rolled twice, 8-byte
-    # keys written, re-sorted and read: 34 B per window) runs at a fraction of
-    # peak, bound by the shared-memory pipe of its dedup sets; the fill
+    # keys written to super-buckets, re-sorted into buckets and read by the
+    # dedup: 34 B per window) runs at a fraction of peak -- its kernels are
+    # issue/latency bound (the histogram's and scatter's rolling, the
+    # scatter's per-key 8-byte stores, the dedup sets' probe loop); the fill
     # (corpus once + the matrix written and copied) is issue-bound on the
     # IMAD pipe (XXH64's 64-bit multiplies).  ncu figures: committed captures.
     peak, _ = measured_peak()
     count_bytes = 34 * windows
     fill_bytes = int(lengths.sum()) + 3 * index_bytes
     out["roofline"] = {
-        "count": {"bound": "shared-memory pipe of the dedup sets (ncu L1/TEX 80 % busy), not HBM",
+        "count": {"bound": "issue/latency (rolling, per-key scattered stores, the dedup probe loop), not HBM",
                   "design_bytes": count_bytes, "achieved_gbs": count_bytes / (c / 1e3) / 1e9,
                   "peak_gbs": peak, "frac": count_bytes / (c / 1e3) / 1e9 / peak,
-                  "ncu": "profiles/r2/count_ab.md (pc_dedup: L1/TEX 80.5 %, issue 48 %; hist issue 63 %)"},
+                  "ncu": "profiles/r2/count_fp (C3 launch list: hist 207, super scatter 451, final 314, "
+                         "dedup 446 ms; dedup wave: issue 57 %, 3 CTAs/SM)"},
         "fill": {"bound": "issue (IMAD pipe: XXH64's 19 64-bit multiplies per window), not HBM",
                  "design_bytes": fill_bytes, "achieved_gbs": fill_bytes / (f / 1e3) / 1e9,
                  "peak_gbs": peak, "frac": fill_bytes / (f / 1e3) / 1e9 / peak,
