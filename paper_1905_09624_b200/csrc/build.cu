@@ -99,6 +99,11 @@ __device__ __forceinline__ void roll_windows(const uint8_t* sb, uint64_t j0, uin
     }
 }
 
+#ifndef COBS_PC_PREFETCH
+#define COBS_PC_PREFETCH 1
+#endif
+constexpr bool kPcPrefetch = COBS_PC_PREFETCH != 0;
+
 // ---- packed rolling for 2-bit DNA codes (the count pass's hot loop) ----
 //
 // 16 bases enter at once: their bytes become 2-bit codes four at a time
@@ -166,8 +171,19 @@ __device__ __forceinline__ void roll_range_packed(const uint8_t* sb, uint64_t j0
         ++i;
     };
     while (i < end && (reinterpret_cast<uintptr_t>(sb + i) & 15u)) push1(__ldg(sb + i));
+    // the 16 bytes after the current ones are loaded while these are rolled
+    // (A/B knob COBS_PC_PREFETCH: C3 super-bucket scatter 451 -> 407 ms, count
+    // 1,510-1,542 -> 1,460-1,470 ms; the histogram pass unchanged)
+    uint4 vn = make_uint4(0u, 0u, 0u, 0u);
+    if (kPcPrefetch && i + 16 <= end) vn = __ldg(reinterpret_cast<const uint4*>(sb + i));
     while (i + 16 <= end) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(sb + i));
+        uint4 v;
+        if (kPcPrefetch) {
+            v = vn;
+            if (i + 32 <= end) vn = __ldg(reinterpret_cast<const uint4*>(sb + i + 16));
+        } else {
+            v = __ldg(reinterpret_cast<const uint4*>(sb + i));
+        }
         const uint32_t P = (pack4(v.x) << 24) | (pack4(v.y) << 16) | (pack4(v.z) << 8) | pack4(v.w);
         uint32_t rp = __brev(P); // complement codes, first base lowest
         rp = ~(((rp >> 1) & 0x55555555u) | ((rp & 0x55555555u) << 1));
@@ -499,6 +515,8 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
         __syncthreads();
         for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] = off[b_lo + t];
         const uint32_t k0 = off[b_lo], k1 = off[b_lo + bps];
+        // (loading the next tile's keys while this one is placed: 122
+        // registers instead of 71, C3 placement 314 -> 360 ms; not kept)
         for (uint32_t tile = k0; tile < k1; tile += kFinTile) {
             const uint32_t n = min(kFinTile, k1 - tile);
             for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cnt[t] = 0;
