@@ -643,33 +643,42 @@ __device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, 
     return false;
 }
 
-// The keys of one bucket, each thread walking i = tid, tid + T, ... with two
-// keys in flight (a and b alternate probes, one probe per key per trip).
-// (A warp-sliced variant refilling lanes by ballot kept more lanes busy but
-// issued more instructions: C3 dedup wave 25.0 vs 23.0 ms.)
+// The keys of one bucket, each thread walking i = tid, tid + T, ... with
+// kDdInFlight keys in flight (each gets one probe per trip; a settled key is
+// replaced by the thread's next one).  (A warp-sliced variant refilling
+// lanes by ballot kept more lanes busy but issued more instructions: C3
+// dedup wave 25.0 vs 23.0 ms.)
+#ifndef COBS_DD_INFLIGHT
+#define COBS_DD_INFLIGHT 2
+#endif
+constexpr int kDdInFlight = COBS_DD_INFLIGHT;
 template <int THREADS, bool SMEM>
 __device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
-                                          uint32_t s_keys,
-                                          const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
+                                          uint32_t s_keys, const unsigned long long* g_keys, uint32_t& mine,
+                                          bool& stuck) {
     uint32_t next = threadIdx.x;
-    DdKey a{0, next, 0}, b{0, next + THREADS, 0};
-    bool la = a.i < n, lb = b.i < n;
-    next += 2 * THREADS;
-    if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
-    if (lb) b.m = dd_key<SMEM>(s_keys, g_keys, b.i);
-    while (la || lb) {
-        if (la && dd_probe<SMEM>(a, sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
-            a = DdKey{0, next, 0};
-            next += THREADS;
-            la = a.i < n;
-            if (la) a.m = dd_key<SMEM>(s_keys, g_keys, a.i);
-        }
-        if (lb && dd_probe<SMEM>(b, sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
-            b = DdKey{0, next, 0};
-            next += THREADS;
-            lb = b.i < n;
-            if (lb) b.m = dd_key<SMEM>(s_keys, g_keys, b.i);
-        }
+    DdKey key[kDdInFlight];
+    bool live[kDdInFlight];
+#pragma unroll
+    for (int j = 0; j < kDdInFlight; ++j) {
+        key[j] = DdKey{0, next, 0};
+        next += THREADS;
+        live[j] = key[j].i < n;
+        if (live[j]) key[j].m = dd_key<SMEM>(s_keys, g_keys, key[j].i);
+    }
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < kDdInFlight; ++j) any |= live[j];
+        if (!any) break;
+#pragma unroll
+        for (int j = 0; j < kDdInFlight; ++j)
+            if (live[j] && dd_probe<SMEM>(key[j], sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
+                key[j] = DdKey{0, next, 0};
+                next += THREADS;
+                live[j] = key[j].i < n;
+                if (live[j]) key[j].m = dd_key<SMEM>(s_keys, g_keys, key[j].i);
+            }
     }
 }
 
