@@ -234,13 +234,14 @@ inline QueryResult query(const GpuIndexView& index, std::string_view pattern, co
 namespace detail {
 inline std::unique_ptr<GpuIndexView> build(const std::vector<Document>& docs, const IndexParams& params, int kind,
                                            uint64_t forced_w, int device) {
-    std::string seqs;
+    // the strings stay where they are: one pointer per string (COBS_B_SEGMENT_PTRS)
+    std::vector<const uint8_t*> seqs;
     std::vector<uint64_t> seg{0}, doc_segs{0};
     std::vector<const char*> names;
     for (const Document& d : docs) {
         for (const std::string& c : d.content) {
-            seqs += c;
-            seg.push_back(seqs.size());
+            seqs.push_back(reinterpret_cast<const uint8_t*>(c.data()));
+            seg.push_back(seg.back() + c.size());
         }
         doc_segs.push_back(seg.size() - 1);
         names.push_back(d.name.c_str());
@@ -249,7 +250,8 @@ inline std::unique_ptr<GpuIndexView> build(const std::vector<Document>& docs, co
     char err[1024];
     cobs_gpu_index* h = nullptr;
     check(cobs_gpu_build_ex(reinterpret_cast<const uint8_t*>(seqs.data()), seg.data(), seg.size() - 1,
-                            doc_segs.data(), names.data(), names.size(), &c, kind, forced_w, device, 0,
+                            doc_segs.data(), names.data(), names.size(), &c, kind, forced_w, device,
+                            COBS_B_SEGMENT_PTRS,
                             nullptr, nullptr, nullptr, &h, err, sizeof err),
           err);
     return std::make_unique<GpuIndexView>(h);

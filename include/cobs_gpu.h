@@ -241,6 +241,13 @@ int cobs_gpu_build(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t n_
  * terms, and a term whose length is not q returns COBS_EUSAGE with the
  * reference's message (classic_index.cpp:49-56). */
 #define COBS_B_TERMS 2u
+/* `seqs` is `const uint8_t* const*`: n_segs host pointers, string i of
+ * seg_offsets[i+1] - seg_offsets[i] bytes (the offsets still describe the
+ * packed layout).  The strings are gathered into HBM through the library's
+ * pinned staging buffers, so a caller holding separate strings (the
+ * reference's vector<string> contents) needs no packed host copy.  Not
+ * with COBS_B_DEVICE_INPUT. */
+#define COBS_B_SEGMENT_PTRS 4u
 
 /* cobs_gpu_build with flags, optionally returning the built index resident
  * in HBM (`index_out`, ready to query; close with cobs_gpu_index_close)

@@ -201,13 +201,14 @@ inline QueryResult query(const DeviceIndexView& index, std::string_view pattern,
 namespace detail {
 inline std::unique_ptr<DeviceIndexView> build(const std::vector<TermSet>& documents, const IndexParams& params,
                                               int kind, uint64_t forced_w, int device) {
-    std::string terms;
+    // the terms stay where they are: one pointer per term (COBS_B_SEGMENT_PTRS)
+    std::vector<const uint8_t*> terms;
     std::vector<uint64_t> seg{0}, doc_segs{0};
     std::vector<const char*> names;
     for (const TermSet& d : documents) {
         for (const std::string& t : d.terms) {
-            terms += t;
-            seg.push_back(terms.size());
+            terms.push_back(reinterpret_cast<const uint8_t*>(t.data()));
+            seg.push_back(seg.back() + t.size());
         }
         doc_segs.push_back(seg.size() - 1);
         names.push_back(d.name.c_str());
@@ -222,7 +223,8 @@ inline std::unique_ptr<DeviceIndexView> build(const std::vector<TermSet>& docume
     char err[1024];
     cobs_gpu_index* h = nullptr;
     check(cobs_gpu_build_ex(reinterpret_cast<const uint8_t*>(terms.data()), seg.data(), seg.size() - 1,
-                            doc_segs.data(), names.data(), names.size(), &c, kind, forced_w, device, COBS_B_TERMS,
+                            doc_segs.data(), names.data(), names.size(), &c, kind, forced_w, device,
+                            COBS_B_TERMS | COBS_B_SEGMENT_PTRS,
                             nullptr, nullptr, nullptr, &h, err, sizeof err),
           err);
     return std::make_unique<DeviceIndexView>(h);

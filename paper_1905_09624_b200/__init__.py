@@ -453,17 +453,20 @@ Document = Tuple[bytes, Sequence[bytes]]  # (name, content strings)
 
 
 def _pack_docs(docs: Sequence[Document]):
+    """Names, one host pointer per content string (COBS_B_SEGMENT_PTRS: the
+    library gathers the strings into HBM itself, no packed copy here), the
+    strings' packed offsets and each document's string range."""
     names, segs, doc_segs = [], [], [0]
     for name, content in docs:
         names.append(name if isinstance(name, bytes) else name.encode())
         for c in content:
-            segs.append(c if isinstance(c, bytes) else c.encode())
+            segs.append(bytes(c) if not isinstance(c, (bytes, str)) else c if isinstance(c, bytes) else c.encode())
         doc_segs.append(len(segs))
     lens = np.fromiter((len(s) for s in segs), dtype=np.uint64, count=len(segs))
     seg_off = np.zeros(len(segs) + 1, dtype=np.uint64)
     np.cumsum(lens, out=seg_off[1:])
-    buf = np.frombuffer(b"".join(segs), dtype=np.uint8) if segs else np.zeros(1, np.uint8)
-    return names, buf, seg_off, np.asarray(doc_segs, dtype=np.uint64)
+    ptrs = (C.c_char_p * max(len(segs), 1))(*segs)  # (keeps the strings alive)
+    return names, ptrs, seg_off, np.asarray(doc_segs, dtype=np.uint64)
 
 
 def build_image(docs: Sequence[Document], params: IndexParams, kind: int, forced_w: int = 0,
@@ -476,10 +479,10 @@ def build_image(docs: Sequence[Document], params: IndexParams, kind: int, forced
     ln = C.c_uint64()
     err = _errbuf()
     cp = params._c()
-    rc = N.lib.cobs_gpu_build(buf.ctypes.data, seg_off.ctypes.data, len(seg_off) - 1,
-                              doc_segs.ctypes.data, name_arr, len(names), C.byref(cp), kind,
-                              forced_w, device, str(path).encode() if path else None,
-                              C.byref(img), C.byref(ln), err, len(err))
+    rc = N.lib.cobs_gpu_build_ex(C.cast(buf, C.c_void_p), seg_off.ctypes.data, len(seg_off) - 1,
+                                 doc_segs.ctypes.data, name_arr, len(names), C.byref(cp), kind,
+                                 forced_w, device, N.B_SEGMENT_PTRS, str(path).encode() if path else None,
+                                 C.byref(img), C.byref(ln), None, err, len(err))
     if rc:
         _raise(rc, err)
     try:
@@ -546,9 +549,9 @@ def build_from_terms(termsets: Sequence[Tuple[bytes, Sequence[bytes]]], params: 
     ln = C.c_uint64()
     err = _errbuf()
     cp = params._c()
-    rc = N.lib.cobs_gpu_build_ex(buf.ctypes.data, seg_off.ctypes.data, len(seg_off) - 1,
+    rc = N.lib.cobs_gpu_build_ex(C.cast(buf, C.c_void_p), seg_off.ctypes.data, len(seg_off) - 1,
                                  doc_segs.ctypes.data, nm, len(names), C.byref(cp), kind, forced_w,
-                                 device, N.B_TERMS, str(path).encode() if path else None,
+                                 device, N.B_TERMS | N.B_SEGMENT_PTRS, str(path).encode() if path else None,
                                  C.byref(img), C.byref(ln), None, err, len(err))
     if rc:
         _raise(rc, err)

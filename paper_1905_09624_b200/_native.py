@@ -126,4 +126,4 @@ for _name, (_res, _args) in SIGNATURES.items():
 
 OK, EUSAGE, EDATA, ECUDA = 0, 1, 2, 4
 Q_HITS, Q_SCORES, Q_DEVICE_INPUT, Q_KEEP_DEVICE, Q_PRUNE = 1, 2, 4, 8, 16
-B_DEVICE_INPUT, B_TERMS = 1, 2
+B_DEVICE_INPUT, B_TERMS, B_SEGMENT_PTRS = 1, 2, 4

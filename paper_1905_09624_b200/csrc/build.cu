@@ -955,7 +955,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                                                 uint64_t n_segs, const uint64_t* doc_segs,
                                                 const std::vector<std::string>& names, const Params& P,
                                                 uint8_t kind, uint64_t forced_w, int device,
-                                                bool seqs_on_device, bool terms_input) {
+                                                bool seqs_on_device, bool terms_input, bool seg_ptrs) {
     auto t_start = std::chrono::steady_clock::now();
     g_timing = BuildTiming();
     P.validate();                                             // params.hpp:26-35
@@ -1034,7 +1034,10 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     d_docstart.reserve(8 * n_docs);
     d_tc.reserve(8 * n_docs);
     auto t_h2d = std::chrono::steady_clock::now();
-    if (!seqs_on_device) h2d_staged(d_seqs.ptr, seqs, total_bytes, st);
+    if (seg_ptrs) // one host pointer per string (COBS_B_SEGMENT_PTRS)
+        h2d_gather_staged(d_seqs.ptr, reinterpret_cast<const uint8_t* const*>(seqs), seg_off, n_segs, st);
+    else if (!seqs_on_device)
+        h2d_staged(d_seqs.ptr, seqs, total_bytes, st);
     COBS_CUDA(cudaMemcpyAsync(d_segoff.ptr, seg_off, 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     COBS_CUDA(cudaMemcpyAsync(d_segw.ptr, seg_rbase.data(), 8 * (n_segs + 1), cudaMemcpyHostToDevice, st));
     if (n_segs)

@@ -30,7 +30,8 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                                                 uint64_t n_segs, const uint64_t* doc_segs,
                                                 const std::vector<std::string>& names, const Params& P,
                                                 uint8_t kind, uint64_t forced_w, int device,
-                                                bool seqs_on_device, bool terms_input = false);
+                                                bool seqs_on_device, bool terms_input = false,
+                                                bool seg_ptrs = false);
 // File image (header + un-pitched payload) of a device-resident index.
 std::vector<uint8_t> index_image(const DeviceIndex& ix);
 // The same into caller memory of index_image_size() bytes (no zero fill).

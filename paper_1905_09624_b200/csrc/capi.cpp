@@ -352,11 +352,14 @@ int cobs_gpu_build_ex(const uint8_t* seqs, const uint64_t* seg_offsets, uint64_t
     if (image_len) *image_len = 0;
     if (index_out) *index_out = nullptr;
     return guarded(err, errlen, [&] {
+        if ((flags & COBS_B_SEGMENT_PTRS) && (flags & COBS_B_DEVICE_INPUT))
+            throw cobsg::UsageError("build: COBS_B_SEGMENT_PTRS needs host strings");
         std::vector<std::string> nm(n_docs);
         for (uint64_t d = 0; d < n_docs; ++d) nm[d] = names[d];
         auto ix = cobsg::build_device_index(seqs, seg_offsets, n_segs, doc_segs, nm, to_params(params),
                                             static_cast<uint8_t>(kind), forced_w, device,
-                                            (flags & COBS_B_DEVICE_INPUT) != 0, (flags & COBS_B_TERMS) != 0);
+                                            (flags & COBS_B_DEVICE_INPUT) != 0, (flags & COBS_B_TERMS) != 0,
+                                            (flags & COBS_B_SEGMENT_PTRS) != 0);
         if (out_path || image) { // the image is made once, straight into the returned buffer
             const auto t0 = std::chrono::steady_clock::now();
             const uint64_t size = cobsg::index_image_size(*ix);

@@ -114,6 +114,42 @@ void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_
         if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // the pool is reused after return
 }
 
+void h2d_gather_staged(void* dst_dev, const uint8_t* const* seg_ptrs, const uint64_t* seg_off, uint64_t n_segs,
+                       cudaStream_t st) {
+    const uint64_t bytes = n_segs ? seg_off[n_segs] - seg_off[0] : 0;
+    if (bytes == 0) return;
+    StagePool& P = stage_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    Event done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+    bool busy[2] = {false, false};
+    uint8_t* dst = static_cast<uint8_t*>(dst_dev);
+    const uint64_t base = seg_off[0];
+    for (uint64_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
+        const int b = static_cast<int>(i & 1);
+        const uint64_t len = std::min(kStageBytes, bytes - off);
+        P.buf[b].reserve(kStageBytes);
+        if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // its last DMA has drained
+        uint8_t* stage = P.buf[b].as<uint8_t>();
+        // packed bytes [off + lo, off + hi) from the strings that hold them
+        host_parallel(len, 8ull << 20, [&](uint64_t lo, uint64_t hi) {
+            uint64_t pos = base + off + lo;
+            const uint64_t end = base + off + hi;
+            uint64_t s = static_cast<uint64_t>(std::upper_bound(seg_off, seg_off + n_segs + 1, pos) - seg_off) - 1;
+            while (pos < end) {
+                const uint64_t take = std::min(end, seg_off[s + 1]) - pos;
+                if (take) std::memcpy(stage + (pos - base - off), seg_ptrs[s] + (pos - seg_off[s]), take);
+                pos += take;
+                ++s;
+            }
+        });
+        COBS_CUDA(cudaMemcpyAsync(dst + off, stage, len, cudaMemcpyHostToDevice, st));
+        COBS_CUDA(cudaEventRecord(done[b], st));
+        busy[b] = true;
+    }
+    for (int b = 0; b < 2; ++b)
+        if (busy[b]) COBS_CUDA(cudaEventSynchronize(done[b])); // the pool is reused after return
+}
+
 void* result_alloc(size_t bytes) {
     constexpr size_t kHuge = 2u << 20;
     if (bytes < kHuge) {

@@ -138,6 +138,10 @@ struct DeviceIndex {
 // (the driver's own pageable path is one thread and a narrow 2D copy engine
 // path is slower still).  Pinned sources/destinations are copied directly.
 void h2d_staged(void* dst_dev, const void* src_host, uint64_t bytes, cudaStream_t st);
+// The packed layout seg_off[0..n_segs] gathered from one host pointer per
+// string (no packed host copy), through the same pinned staging pair.
+void h2d_gather_staged(void* dst_dev, const uint8_t* const* seg_ptrs, const uint64_t* seg_off, uint64_t n_segs,
+                       cudaStream_t st);
 // Device -> pageable host through the same pinned pair, host threads copying
 // chunk i out while chunk i+1 is in flight (the driver's pageable D2H path
 // runs at ~2 GB/s into freshly allocated memory).  Synchronous.
