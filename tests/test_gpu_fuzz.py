@@ -2,8 +2,9 @@
 parameters (q 1-40, k 1-4, p, canonical, classic/compact, block size), random
 alphabets (DNA with N and lowercase, protein, arbitrary bytes), random
 document and pattern shapes.  Every iteration: the GPU-built file equals the
-oracle's byte for byte, and the batch's l, skipped, status, dense scores and
-ordered, top_t-cut hit lists equal the oracle's."""
+oracle's byte for byte (with the default count and with the partitioned
+count under random knobs), and the batch's l, skipped, status, dense scores
+and ordered, top_t-cut hit lists equal the oracle's."""
 import os
 import random
 
@@ -40,10 +41,26 @@ def test_fuzz_build_and_query(gpu, it):
         segs = [rbytes(rng, rng.choice([0, rng.randint(1, 40), rng.randint(40, 900)]), alphabet)
                 for _ in range(rng.randint(1, 3))]
         docs.append((b"f%04d" % names[i], segs))
-    img = cb.build_image(docs, cb.IndexParams(q=q, k=k, p=p, canonical=canonical, block_size=B), kind,
-                         device=gpu)
+    params = cb.IndexParams(q=q, k=k, p=p, canonical=canonical, block_size=B)
+    img = cb.build_image(docs, params, kind, device=gpu)
     assert img == O.build_image(docs, q=q, k=k, p=p, canonical=canonical, block_size=B, kind=kind), \
         (it, q, k, canonical, kind, B)
+    # the partitioned count (2-bit / symbol codes, fingerprint dedup sets) on
+    # the same corpus, with random bucket sizes, narrowed fingerprints and
+    # small waves -- the corpora are below its size threshold, so forced
+    knobs = {"COBS_COUNT_PARTITION": "1", "COBS_PC_TARGET": str(rng.choice([64, 300, 4096])),
+             "COBS_PC_FP_MASK": rng.choice(["0xffffffff", "0x30000", "0x0"]),
+             "COBS_PC_WAVE_KEYS": str(rng.choice([2000, 1 << 30]))}
+    saved = {v: os.environ.get(v) for v in knobs}
+    os.environ.update(knobs)
+    try:
+        assert cb.build_image(docs, params, kind, device=gpu) == img, (it, knobs)
+    finally:
+        for v, old in saved.items():
+            if old is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = old
     view = cb.open_image(img, gpu)
     idx = O.OracleIndex.parse(img)
     pats = []
