@@ -1204,24 +1204,47 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 max_nsup = std::max(max_nsup, wv.nsup);
                 max_nchunk = std::max(max_nchunk, wv.nchunk);
             }
-            DevBuf d_keys, d_keys_a, d_sup_cur, d_sup_doc, d_docs, d_cnt, d_off, d_flags, d_tmp, d_bdoc, d_chunk_sup;
+            // Wave i's histogram pass (+ scan, super-bucket cursors) runs on a
+            // second stream while wave i-1 is scattered and deduplicated, so
+            // its rolling overlaps their memory/latency-bound kernels; the
+            // per-wave arrays are double-buffered (A/B knob COBS_PC_OVERLAP=0).
+            const auto t_alloc = std::chrono::steady_clock::now();
+            const char* ov_env = std::getenv("COBS_PC_OVERLAP");
+            const bool overlap = !(ov_env && ov_env[0] == '0');
+            DevBuf d_keys, d_keys_a, d_docs, d_flags;
+            DevBuf d_sup_cur[2], d_sup_doc[2], d_cnt[2], d_off[2], d_tmp[2], d_bdoc[2], d_chunk_sup[2];
             d_keys.reserve(8 * max_keys + 16); // (+16: the dedup's 16-byte staged copies may read one key past the end)
             d_keys_a.reserve(8 * max_keys);
-            d_chunk_sup.reserve(4ull * kSup * max_nchunk);
-            d_sup_cur.reserve(4 * max_nsup);
-            d_sup_doc.reserve(4 * max_nsup);
             d_flags.reserve(16 * std::max<size_t>(pw.size(), 1));
-            d_cnt.reserve(4 * (max_nbuck + 1));
-            d_off.reserve(4 * (max_nbuck + 1));
-            d_bdoc.reserve(4 * (max_nbuck + 1));
             d_docs.reserve(sizeof(PcDoc) * std::max<size_t>(pd.size(), 1));
             size_t tmp_bytes = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt.as<uint32_t>(), d_off.as<uint32_t>(),
-                                          static_cast<int>(max_nbuck + 1), st);
-            d_tmp.reserve(std::max<size_t>(tmp_bytes, 16));
+            for (int b = 0; b < (overlap ? 2 : 1); ++b) {
+                d_chunk_sup[b].reserve(4ull * kSup * max_nchunk);
+                d_sup_cur[b].reserve(4 * max_nsup);
+                d_sup_doc[b].reserve(4 * max_nsup);
+                d_cnt[b].reserve(4 * (max_nbuck + 1));
+                d_off[b].reserve(4 * (max_nbuck + 1));
+                d_bdoc[b].reserve(4 * (max_nbuck + 1));
+                cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt[b].as<uint32_t>(), d_off[b].as<uint32_t>(),
+                                              static_cast<int>(max_nbuck + 1), st);
+                d_tmp[b].reserve(std::max<size_t>(tmp_bytes, 16));
+            }
+            g_timing.ms_count_alloc = ms_since(t_alloc);
             if (!pd.empty())
                 COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
             COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
+            cudaStream_t hs = st;
+            if (overlap) COBS_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+            struct HsGuard {
+                cudaStream_t s, main;
+                ~HsGuard() {
+                    if (s != main) cudaStreamDestroy(s);
+                }
+            } hsg{hs, st};
+            Event ev_ready(cudaEventDisableTiming), ev_hist[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)},
+                  ev_done[2] = {Event(cudaEventDisableTiming), Event(cudaEventDisableTiming)};
+            COBS_CUDA(cudaEventRecord(ev_ready, st));
+            COBS_CUDA(cudaStreamWaitEvent(hs, ev_ready, 0));
             auto hist = sym_bits ? pc_hist_kernel<0, kSymBits> : q == 31 ? pc_hist_kernel<31> : pc_hist_kernel<0>;
             auto scat = sym_bits ? pc_scatter_super_kernel<0, kSymBits>
                         : q == 31 ? pc_scatter_super_kernel<31> : pc_scatter_super_kernel<0>;
@@ -1240,40 +1263,47 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                                               : 0xffffffffu;
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
+                if (!wv.nchunk) continue;
+                const int b = overlap ? static_cast<int>(i & 1) : 0;
                 const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
                 unsigned long long* flags = d_flags.as<unsigned long long>() + 2 * i;
-                COBS_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 4 * (wv.nbuck + 1), st));
-                pc_bdoc_kernel<<<std::min<uint32_t>(nd, 148 * 8), 256, 0, st>>>(d_docs.as<PcDoc>() + wv.doc0, nd,
-                                                                               d_bdoc.as<uint32_t>());
                 PcArgs pa{};
                 pa.a = wa;
                 pa.docs = d_docs.as<PcDoc>() + wv.doc0;
                 pa.ndocs = nd;
                 pa.nchunks = wv.nchunk;
-                pa.bucket_cnt = d_cnt.as<uint32_t>();
+                pa.bucket_cnt = d_cnt[b].as<uint32_t>();
                 pa.keys = d_keys_a.as<unsigned long long>();
                 pa.bad = flags;
-                pa.chunk_sup = d_chunk_sup.as<uint32_t>();
+                pa.chunk_sup = d_chunk_sup[b].as<uint32_t>();
                 pa.symtab = d_symtab.as<uint8_t>();
-                if (!wv.nchunk) continue;
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
-                hist<<<grid, 256, 0, st>>>(pa);
-                size_t tb = d_tmp.bytes;
-                COBS_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.ptr, tb, d_cnt.as<uint32_t>(), d_off.as<uint32_t>(),
-                                                        static_cast<int>(wv.nbuck + 1), st));
-                pc_super_init_kernel<<<std::min<uint32_t>(nd, 148 * 8), kSup, 0, st>>>(
-                    d_docs.as<PcDoc>() + wv.doc0, nd, d_off.as<uint32_t>(), d_sup_cur.as<uint32_t>(),
-                    d_sup_doc.as<uint32_t>());
-                scat<<<grid, 256, 0, st>>>(pa, d_sup_cur.as<uint32_t>());
+                // histogram side (buffers b are free once wave i-2's dedup is done)
+                COBS_CUDA(cudaStreamWaitEvent(hs, ev_done[b], 0));
+                COBS_CUDA(cudaMemsetAsync(d_cnt[b].ptr, 0, 4 * (wv.nbuck + 1), hs));
+                pc_bdoc_kernel<<<std::min<uint32_t>(nd, 148 * 8), 256, 0, hs>>>(d_docs.as<PcDoc>() + wv.doc0, nd,
+                                                                               d_bdoc[b].as<uint32_t>());
+                hist<<<grid, 256, 0, hs>>>(pa);
+                size_t tb = d_tmp[b].bytes;
+                COBS_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp[b].ptr, tb, d_cnt[b].as<uint32_t>(), d_off[b].as<uint32_t>(),
+                                                        static_cast<int>(wv.nbuck + 1), hs));
+                pc_super_init_kernel<<<std::min<uint32_t>(nd, 148 * 8), kSup, 0, hs>>>(
+                    d_docs.as<PcDoc>() + wv.doc0, nd, d_off[b].as<uint32_t>(), d_sup_cur[b].as<uint32_t>(),
+                    d_sup_doc[b].as<uint32_t>());
+                COBS_CUDA(cudaEventRecord(ev_hist[b], hs));
+                // key side
+                COBS_CUDA(cudaStreamWaitEvent(st, ev_hist[b], 0));
+                scat<<<grid, 256, 0, st>>>(pa, d_sup_cur[b].as<uint32_t>());
                 pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
-                    d_docs.as<PcDoc>() + wv.doc0, d_sup_doc.as<uint32_t>(), wv.nsup, d_off.as<uint32_t>(),
+                    d_docs.as<PcDoc>() + wv.doc0, d_sup_doc[b].as<uint32_t>(), wv.nsup, d_off[b].as<uint32_t>(),
                     d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
                 const uint64_t kcap = std::min<uint64_t>(wv.kcap, ((227 * 1024 - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
                 dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dd512 ? 512 : 256,
                         dd_smem(wv.slots, kcap), st>>>(
-                    d_off.as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc.as<uint32_t>(),
+                    d_off[b].as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc[b].as<uint32_t>(),
                     d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
                     static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf, fp_test_mask);
+                COBS_CUDA(cudaEventRecord(ev_done[b], st));
                 COBS_CUDA(cudaGetLastError());
             }
             g_timing.count_waves = static_cast<uint32_t>(pw.size());
@@ -1347,8 +1377,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         cudaEventElapsedTime(&ms_count, e0, e1);
         g_timing.ms_count = ms_count;
         if (std::getenv("COBS_BUILD_DEBUG"))
-            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u\n",
-                         ms_count, use_pc ? 1 : 0, g_timing.count_waves, g_timing.count_fallback_waves, fill_rpt);
+            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u alloc=%.1f ms\n",
+                         ms_count, use_pc ? 1 : 0, g_timing.count_waves, g_timing.count_fallback_waves, fill_rpt,
+                         g_timing.ms_count_alloc);
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
     }
 

@@ -13,6 +13,7 @@ namespace cobsg {
 struct BuildTiming {
     double ms_h2d = 0, ms_count = 0, ms_fill = 0, ms_d2h = 0, ms_total = 0;
     uint32_t count_waves = 0, count_fallback_waves = 0; // partitioned count: waves, recounted waves
+    double ms_count_alloc = 0; // host time of the partitioned count's buffer allocation (debug)
 };
 const BuildTiming& last_build_timing();
 
