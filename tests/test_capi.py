@@ -113,3 +113,22 @@ def test_build_usage_errors_without_device():
         cb.build_classic([(b"a", [b"ACGT" * 10])], cb.IndexParams(k=0))
     with pytest.raises(cb.DataError, match="duplicate document name: x"):
         cb.build_compact([(b"x", [b"ACGT" * 10]), (b"x", [b"ACGT" * 10])])
+
+
+def test_build_segment_ptrs_rejects_device_input():
+    """COBS_B_SEGMENT_PTRS (host pointer per string) with COBS_B_DEVICE_INPUT
+    is a usage error, reported before any device call; the Python packer
+    hands the library one pointer per string (no packed copy)."""
+    import paper_1905_09624_b200 as cb
+    from paper_1905_09624_b200 import _native as N
+    names, ptrs, seg_off, doc_segs = cb._pack_docs([(b"a", [b"ACGT" * 10, b"GG"]), ("b", ["TTTT" * 9])])
+    assert [C.string_at(ptrs[i], int(seg_off[i + 1] - seg_off[i])) for i in range(3)] == \
+        [b"ACGT" * 10, b"GG", b"TTTT" * 9]
+    assert list(doc_segs) == [0, 2, 3] and names == [b"a", b"b"]
+    nm = (C.c_char_p * 2)(*names)
+    err = C.create_string_buffer(512)
+    cp = cb.IndexParams()._c()
+    rc = N.lib.cobs_gpu_build_ex(C.cast(ptrs, C.c_void_p), seg_off.ctypes.data, 3, doc_segs.ctypes.data, nm, 2,
+                                 C.byref(cp), cb.KIND_CLASSIC, 0, 0, N.B_SEGMENT_PTRS | N.B_DEVICE_INPUT, None,
+                                 None, None, None, err, len(err))
+    assert rc == 1 and b"COBS_B_SEGMENT_PTRS" in err.value
