@@ -937,6 +937,14 @@ __global__ void unit_copy_kernel(const CopyUnit* units, const uint64_t* prefix, 
     }
 }
 
+// a sub-range of a DevBuf
+struct BufView {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
 inline uint64_t next_pow2(uint64_t x) {
     uint64_t p = 2;
     while (p < x) p <<= 1;
@@ -1068,6 +1076,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
     uint64_t slab_wave_bytes = 96ull << 20;
     if (const char* e = std::getenv("COBS_SLAB_WAVE_MB")) slab_wave_bytes = std::strtoull(e, nullptr, 10) << 20;
     std::vector<uint64_t> tc(n_docs);
+    std::chrono::steady_clock::time_point t_count0 = std::chrono::steady_clock::now();
     uint32_t fill_rpt = 1; // kFillRunsDna once the count has seen only 2-bit-code windows
     if (terms_input) { // TermSet::term_count() = terms.size() (termizer.hpp:25)
         for (uint64_t d = 0; d < n_docs; ++d) tc[d] = doc_segs[d + 1] - doc_segs[d];
@@ -1211,23 +1220,33 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             const auto t_alloc = std::chrono::steady_clock::now();
             const char* ov_env = std::getenv("COBS_PC_OVERLAP");
             const bool overlap = !(ov_env && ov_env[0] == '0');
-            DevBuf d_keys, d_keys_a, d_docs, d_flags;
-            DevBuf d_sup_cur[2], d_sup_doc[2], d_cnt[2], d_off[2], d_tmp[2], d_bdoc[2], d_chunk_sup[2];
+            DevBuf d_keys, d_keys_a, d_small;
             d_keys.reserve(8 * max_keys + 16); // (+16: the dedup's 16-byte staged copies may read one key past the end)
             d_keys_a.reserve(8 * max_keys);
-            d_flags.reserve(16 * std::max<size_t>(pw.size(), 1));
-            d_docs.reserve(sizeof(PcDoc) * std::max<size_t>(pd.size(), 1));
+            // the per-wave arrays: views into one allocation (one cudaMalloc / cudaFree instead of ~20)
+            BufView d_docs, d_flags, d_sup_cur[2], d_sup_doc[2], d_cnt[2], d_off[2], d_tmp[2], d_bdoc[2], d_chunk_sup[2];
             size_t tmp_bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                          static_cast<int>(max_nbuck + 1), st);
+            std::vector<std::pair<BufView*, size_t>> plan{{&d_flags, 16 * std::max<size_t>(pw.size(), 1)},
+                                                       {&d_docs, sizeof(PcDoc) * std::max<size_t>(pd.size(), 1)}};
             for (int b = 0; b < (overlap ? 2 : 1); ++b) {
-                d_chunk_sup[b].reserve(4ull * kSup * max_nchunk);
-                d_sup_cur[b].reserve(4 * max_nsup);
-                d_sup_doc[b].reserve(4 * max_nsup);
-                d_cnt[b].reserve(4 * (max_nbuck + 1));
-                d_off[b].reserve(4 * (max_nbuck + 1));
-                d_bdoc[b].reserve(4 * (max_nbuck + 1));
-                cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt[b].as<uint32_t>(), d_off[b].as<uint32_t>(),
-                                              static_cast<int>(max_nbuck + 1), st);
-                d_tmp[b].reserve(std::max<size_t>(tmp_bytes, 16));
+                plan.push_back({&d_chunk_sup[b], 4ull * kSup * max_nchunk});
+                plan.push_back({&d_sup_cur[b], 4 * max_nsup});
+                plan.push_back({&d_sup_doc[b], 4 * max_nsup});
+                plan.push_back({&d_cnt[b], 4 * (max_nbuck + 1)});
+                plan.push_back({&d_off[b], 4 * (max_nbuck + 1)});
+                plan.push_back({&d_bdoc[b], 4 * (max_nbuck + 1)});
+                plan.push_back({&d_tmp[b], std::max<size_t>(tmp_bytes, 16)});
+            }
+            size_t arena = 0;
+            for (auto& v : plan) arena += (v.second + 255) & ~size_t(255);
+            d_small.reserve(arena);
+            size_t o = 0;
+            for (auto& v : plan) {
+                v.first->ptr = static_cast<uint8_t*>(d_small.ptr) + o;
+                v.first->bytes = v.second;
+                o += (v.second + 255) & ~size_t(255);
             }
             g_timing.ms_count_alloc = ms_since(t_alloc);
             if (!pd.empty())
@@ -1311,8 +1330,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             if (!pw.empty())
                 COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 16 * pw.size(), cudaMemcpyDeviceToHost, st));
             COBS_CUDA(cudaStreamSynchronize(st));
+            g_timing.ms_count_sync = ms_since(t_count0);
+            const auto t_free = std::chrono::steady_clock::now();
             d_keys.release(); // before any recount needs the memory
             d_keys_a.release();
+            g_timing.ms_count_free = ms_since(t_free);
             bool byte_windows = !oversize.empty() || sym_bits; // symbol-coded windows hash their bytes in the fill
             for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
             if (!byte_windows) fill_rpt = kFillRunsDna;
@@ -1326,6 +1348,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         };
 
         COBS_CUDA(cudaEventRecord(e0, st));
+        t_count0 = std::chrono::steady_clock::now();
         const char* pc_env = std::getenv("COBS_COUNT_PARTITION");
         // (small corpora: the hash sets are L2-resident anyway and need no
         // key buffer; COBS_COUNT_PARTITION=1 forces the partitioned count)
@@ -1377,9 +1400,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         cudaEventElapsedTime(&ms_count, e0, e1);
         g_timing.ms_count = ms_count;
         if (std::getenv("COBS_BUILD_DEBUG"))
-            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u alloc=%.1f ms\n",
+            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u alloc=%.1f sync=%.1f free=%.1f ms\n",
                          ms_count, use_pc ? 1 : 0, g_timing.count_waves, g_timing.count_fallback_waves, fill_rpt,
-                         g_timing.ms_count_alloc);
+                         g_timing.ms_count_alloc, g_timing.ms_count_sync, g_timing.ms_count_free);
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
     }
 

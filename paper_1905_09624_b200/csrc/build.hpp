@@ -14,6 +14,7 @@ struct BuildTiming {
     double ms_h2d = 0, ms_count = 0, ms_fill = 0, ms_d2h = 0, ms_total = 0;
     uint32_t count_waves = 0, count_fallback_waves = 0; // partitioned count: waves, recounted waves
     double ms_count_alloc = 0; // host time of the partitioned count's buffer allocation (debug)
+    double ms_count_sync = 0, ms_count_free = 0; // host: count start -> kernels done, key buffer frees (debug)
 };
 const BuildTiming& last_build_timing();
 
