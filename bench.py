@@ -599,14 +599,15 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
         "count": {"bound": "issue/latency (rolling, per-key scattered stores, the dedup probe loop), not HBM",
                   "design_bytes": count_bytes, "achieved_gbs": count_bytes / (c / 1e3) / 1e9,
                   "peak_gbs": peak, "frac": count_bytes / (c / 1e3) / 1e9 / peak,
-                  "ncu": "profiles/r2/count_fp (C3 launch list: hist 207, super scatter 451, final 314, "
-                         "dedup 446 ms; dedup wave: issue 57 %, 3 CTAs/SM)"},
+                  "ncu": "profiles/r2/count_fp (C3 launch list, serialised: hist 207, super scatter 407, "
+                         "final 314, dedup 446 ms; the histogram pass overlaps the previous wave; "
+                         "dedup wave: issue 57 %, 3 CTAs/SM)"},
         "fill": {"bound": "issue (IMAD pipe: XXH64's 19 64-bit multiplies per window), not HBM",
                  "design_bytes": fill_bytes, "achieved_gbs": fill_bytes / (f / 1e3) / 1e9,
                  "peak_gbs": peak, "frac": fill_bytes / (f / 1e3) / 1e9 / peak,
-                 "issue_active_frac": 0.745,
-                 "ncu": "profiles/r1/build_fill_wave_c3_details.csv (slab_fill_kernel, one C3 wave: 74.5 % issue "
-                        "active, math-pipe throttle the top stall)"}}
+                 "issue_active_frac": 0.71,
+                 "ncu": "profiles/r2/fill_c3_mix.md (slab_fill_kernel, one C3 wave: 71 % issue slots busy, "
+                        "288 instructions per window; round 1: 74.5 %, profiles/r1/build_fill_wave_c3_details.csv)"}}
     try:
         out["cpu_reference"] = cpu_reference_build(cfg, synth, BUILD_CPU_SAMPLE[name])
     except Exception as e:
