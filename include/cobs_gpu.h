@@ -276,6 +276,10 @@ int cobs_gpu_build_timing(double* ms_count, double* ms_fill, double* ms_total);
  * (0 when the index stayed in HBM). */
 int cobs_gpu_build_timing_ex(double* ms_h2d, double* ms_count, double* ms_fill, double* ms_d2h,
                              double* ms_total);
+/* The count leg of the last build split up: its kernels alone (CUDA events
+ * after the workspace allocation and before its release), and the host time
+ * of the workspace's cudaMalloc and cudaFree calls (both inside ms_count). */
+int cobs_gpu_build_timing_count(double* ms_kernels, double* ms_alloc, double* ms_free);
 
 void cobs_gpu_free(void* p);
 

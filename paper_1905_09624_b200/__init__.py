@@ -638,4 +638,8 @@ def last_build_timing_ex() -> dict:
     """ms of the last build's legs: h2d, count, fill, d2h, total."""
     v = [C.c_double() for _ in range(5)]
     N.lib.cobs_gpu_build_timing_ex(*(C.byref(x) for x in v))
-    return dict(zip(("ms_h2d", "ms_count", "ms_fill", "ms_d2h", "ms_total"), (x.value for x in v)))
+    t = dict(zip(("ms_h2d", "ms_count", "ms_fill", "ms_d2h", "ms_total"), (x.value for x in v)))
+    w = [C.c_double() for _ in range(3)]  # the count leg: kernels alone, workspace cudaMalloc / cudaFree
+    N.lib.cobs_gpu_build_timing_count(*(C.byref(x) for x in w))
+    t.update(zip(("ms_count_kernels", "ms_count_alloc", "ms_count_free"), (x.value for x in w)))
+    return t

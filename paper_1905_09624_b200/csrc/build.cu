@@ -319,6 +319,7 @@ constexpr uint32_t kPcHist = 8192;   // buckets a chunk histogram keeps in share
 constexpr uint64_t kPcTarget = 4096;    // keys per bucket: nbk = next_pow2(ceil(W / kPcTarget)) <= kPcHist
                                         // (A/B, fingerprint sets: 2,048 / 3,072 / 4,096 / 8,192 -> C3 count
                                         // 1.78-1.91 / 1.49-1.52 / 1.41-1.50 / 1.74-1.78 s)
+constexpr uint64_t kPcWaveKeys = 1000000000; // windows per wave (A/B knob COBS_PC_WAVE_KEYS)
 constexpr uint32_t kPcMaxSlotsFp = 32768;  // largest fingerprint set (128 KB of shared memory)
                                         // (A/B with 1x-mean sets: 1,024 / 2,048 / 4,096 -> C3 count 1.81 / 1.65 / 1.61 s)
 
@@ -1147,9 +1148,17 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         // bucket too skewed for its set is recounted by hashset_count
         auto partitioned_count = [&] {
             COBS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            // two key buffers (super-bucket scatter, final placement), 16 bytes per window
-            uint64_t kmax = std::min<uint64_t>((free_b / 2) / 16, 0xffffffffull);
-            if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmax, std::strtoull(e, nullptr, 10));
+            // two key buffers (super-bucket scatter, final placement), 16 bytes
+            // per window.  A wave holds <= kPcWaveKeys windows (16 GB of key
+            // buffers): the kernels' time does not depend on the wave size
+            // (C3: 1,316-1,320 ms with 85 GB / 20 waves, 1,327-1,333 ms with
+            // 16 GB / 73 waves), but cudaFree of the 85 GB took 500+ ms on
+            // about one build in five (6-20 ms otherwise; profiles/r2/free_timing)
+            // against 6-8 ms for 16 GB, and the caller keeps its HBM.
+            // (a document larger than that still gets a wave of its own while it fits half the free HBM)
+            const uint64_t kmem = std::min<uint64_t>((free_b / 2) / 16, 0xffffffffull);
+            uint64_t kmax = std::min(kmem, std::max(kPcWaveKeys, doc_w.empty() ? 0 : *std::max_element(doc_w.begin(), doc_w.end())));
+            if (const char* e = std::getenv("COBS_PC_WAVE_KEYS")) kmax = std::min<uint64_t>(kmem, std::strtoull(e, nullptr, 10));
             kmax = std::max<uint64_t>(kmax, 1);
             uint64_t target = kPcTarget; // keys per bucket (A/B knob COBS_PC_TARGET)
             if (const char* e = std::getenv("COBS_PC_TARGET")) target = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
@@ -1249,6 +1258,8 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 o += (v.second + 255) & ~size_t(255);
             }
             g_timing.ms_count_alloc = ms_since(t_alloc);
+            Event ek0, ek1; // the kernels alone: after the allocation, before the frees
+            COBS_CUDA(cudaEventRecord(ek0, st));
             if (!pd.empty())
                 COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
             COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
@@ -1329,7 +1340,13 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             std::vector<uint64_t> flags(2 * pw.size());
             if (!pw.empty())
                 COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 16 * pw.size(), cudaMemcpyDeviceToHost, st));
+            COBS_CUDA(cudaEventRecord(ek1, st));
             COBS_CUDA(cudaStreamSynchronize(st));
+            {
+                float ms_k = 0;
+                cudaEventElapsedTime(&ms_k, ek0, ek1);
+                g_timing.ms_count_kernels = ms_k;
+            }
             g_timing.ms_count_sync = ms_since(t_count0);
             const auto t_free = std::chrono::steady_clock::now();
             d_keys.release(); // before any recount needs the memory
@@ -1338,6 +1355,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             bool byte_windows = !oversize.empty() || sym_bits; // symbol-coded windows hash their bytes in the fill
             for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
             if (!byte_windows) fill_rpt = kFillRunsDna;
+            const auto t_recount = std::chrono::steady_clock::now();
             for (size_t i = 0; i < pw.size(); ++i)
                 if (flags[2 * i] || (flags[2 * i + 1] & 0xffffffffull)) { // recount this wave exactly
                     COBS_CUDA(cudaMemsetAsync(d_tc.as<unsigned long long>() + pw[i].d0, 0, 8 * (pw[i].d1 - pw[i].d0), st));
@@ -1345,6 +1363,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     ++g_timing.count_fallback_waves;
                 }
             for (const auto& r : oversize) hashset_count(r.first, r.second);
+            if (g_timing.count_fallback_waves || !oversize.empty()) g_timing.ms_count_kernels += ms_since(t_recount);
         };
 
         COBS_CUDA(cudaEventRecord(e0, st));
@@ -1399,10 +1418,12 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         float ms_count = 0;
         cudaEventElapsedTime(&ms_count, e0, e1);
         g_timing.ms_count = ms_count;
+        if (!use_pc) g_timing.ms_count_kernels = ms_count; // (hash sets: small tables, allocation included)
         if (std::getenv("COBS_BUILD_DEBUG"))
-            std::fprintf(stderr, "[cobs build] count %.1f ms: partitioned=%d waves=%u recounted=%u fill_rpt=%u alloc=%.1f sync=%.1f free=%.1f ms\n",
-                         ms_count, use_pc ? 1 : 0, g_timing.count_waves, g_timing.count_fallback_waves, fill_rpt,
-                         g_timing.ms_count_alloc, g_timing.ms_count_sync, g_timing.ms_count_free);
+            std::fprintf(stderr, "[cobs build] count %.1f ms (kernels %.1f): partitioned=%d waves=%u recounted=%u fill_rpt=%u alloc=%.1f sync=%.1f free=%.1f ms\n",
+                         ms_count, g_timing.ms_count_kernels, use_pc ? 1 : 0, g_timing.count_waves,
+                         g_timing.count_fallback_waves, fill_rpt, g_timing.ms_count_alloc, g_timing.ms_count_sync,
+                         g_timing.ms_count_free);
         COBS_CUDA(cudaMemcpy(tc.data(), d_tc.ptr, 8 * n_docs, cudaMemcpyDeviceToHost));
     }
 

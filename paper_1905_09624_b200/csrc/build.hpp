@@ -15,6 +15,7 @@ struct BuildTiming {
     uint32_t count_waves = 0, count_fallback_waves = 0; // partitioned count: waves, recounted waves
     double ms_count_alloc = 0; // host time of the partitioned count's buffer allocation (debug)
     double ms_count_sync = 0, ms_count_free = 0; // host: count start -> kernels done, key buffer frees (debug)
+    double ms_count_kernels = 0; // the count's kernels alone (CUDA events: after the buffer allocation, before the frees)
 };
 const BuildTiming& last_build_timing();
 

@@ -453,6 +453,14 @@ int cobs_gpu_build_timing_ex(double* ms_h2d, double* ms_count, double* ms_fill, 
     return COBS_OK;
 }
 
+int cobs_gpu_build_timing_count(double* ms_kernels, double* ms_alloc, double* ms_free) {
+    const cobsg::BuildTiming& t = cobsg::last_build_timing();
+    if (ms_kernels) *ms_kernels = t.ms_count_kernels;
+    if (ms_alloc) *ms_alloc = t.ms_count_alloc;
+    if (ms_free) *ms_free = t.ms_count_free;
+    return COBS_OK;
+}
+
 void cobs_gpu_free(void* p) { std::free(p); }
 
 int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size, double median,
