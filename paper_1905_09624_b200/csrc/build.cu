@@ -602,6 +602,13 @@ __device__ __forceinline__ unsigned long long dd_key(uint32_t s_base, const unsi
     }
 }
 
+// A key's fingerprint: its bits [16 + ib, 47) under fmask (= ~imask; tests
+// narrow it) with bit 31 set, so it is never 0 (an empty slot) and above
+// every index mask (ib <= 28).
+__device__ __forceinline__ uint32_t dd_fp(unsigned long long m, uint32_t fmask) {
+    return (static_cast<uint32_t>(m >> 16) & fmask) | 0x80000000u;
+}
+
 // One probe of a key of the fingerprint set (see pc_dedup_fp_kernel):
 // returns true once the key is settled (new -> ++mine, duplicate, or
 // stuck = every group full).
@@ -613,8 +620,7 @@ template <bool SMEM>
 __device__ __forceinline__ bool dd_probe(DdKey& k, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
                                          uint32_t s_keys,
                                          const unsigned long long* g_keys, uint32_t& mine, bool& stuck) {
-    uint32_t fp = static_cast<uint32_t>(k.m >> 16) & fmask; // (fmask = ~imask; tests narrow it)
-    fp = fp ? fp : imask + 1u;
+    const uint32_t fp = dd_fp(k.m, fmask);
     const uint32_t gaddr = sg + 16u * ((static_cast<uint32_t>(k.m) + k.probes) & gmask);
     uint4 v;
     asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(gaddr));
@@ -683,6 +689,99 @@ __device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmas
     }
 }
 
+// The same for a staged bucket, first probes as straight-line code: each
+// thread takes kDdU keys per step (i = base + u * T), loads their groups
+// back to back, and claims the first empty slot of a group that shows no
+// equal fingerprint with one CAS.  Everything else -- an equal fingerprint
+// (a duplicate or an accident), a full group, a lost CAS (another key took
+// the slot after the group was read; also a second key of this thread in the
+// same group, whose view is stale) -- is left pending: its index goes to the
+// warp's queue in shared memory, and whenever 32 are queued the warp settles
+// them with the probe loop of dd_probe, one per lane (settling each thread's
+// own pending keys right after the step ran that loop at ~15 % lane
+// activity and was slower than the per-key loop: C3 count 1,498 vs 1,328
+// ms).  Exact by the same invariant:
+// slots of a group fill in order, and a CAS on slot s is only tried by a
+// thread that saw the slots before s occupied and unequal, so it succeeds
+// only if nothing was inserted into the group since the thread read it.
+// (C3 dedup wave: 4.1 warp instructions per key in the per-key loop, 21 of
+// 32 lanes active; here all lanes run the first probe.)
+#ifndef COBS_DD_U
+#define COBS_DD_U 1
+#endif
+constexpr int kDdU = COBS_DD_U;
+constexpr uint32_t kDdQueue = 32u * kDdU + 32u; // pending keys a warp can hold (u16 indices)
+template <int THREADS, bool SMEM>
+__device__ __forceinline__ void dd_bucket_fast(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
+                                               uint32_t s_keys, const unsigned long long* g_keys, uint16_t* s_queue,
+                                               uint32_t& mine, bool& stuck) {
+    const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    uint16_t* q = s_queue + (threadIdx.x >> 5) * kDdQueue;
+    uint32_t qn = 0; // (warp-uniform)
+    auto settle = [&](uint32_t i) {
+        DdKey k{dd_key<SMEM>(s_keys, g_keys, i), i, 0};
+        while (!dd_probe<SMEM>(k, sg, gmask, imask, fmask, s_keys, g_keys, mine, stuck)) {
+        }
+    };
+    // keys of step `b` (clamped: a valid address; not used beyond n); keys read
+    // from global memory are loaded one step ahead
+    auto load = [&](uint32_t b, unsigned long long (&k)[kDdU]) {
+#pragma unroll
+        for (int u = 0; u < kDdU; ++u) k[u] = dd_key<SMEM>(s_keys, g_keys, min(b + u * THREADS, n - 1u));
+    };
+    unsigned long long nxt[kDdU];
+    if (!SMEM) load(threadIdx.x, nxt);
+    for (uint32_t wbase = threadIdx.x - lane; wbase < n; wbase += kDdU * THREADS) { // (warp-uniform trip count)
+        const uint32_t base = wbase + lane;
+        unsigned long long m[kDdU];
+        uint32_t ga[kDdU];
+        uint4 v[kDdU];
+        if (SMEM) {
+            load(base, m);
+        } else {
+#pragma unroll
+            for (int u = 0; u < kDdU; ++u) m[u] = nxt[u];
+            load(base + kDdU * THREADS, nxt);
+        }
+#pragma unroll
+        for (int u = 0; u < kDdU; ++u) {
+            ga[u] = sg + 16u * (static_cast<uint32_t>(m[u]) & gmask);
+            asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                         : "r"(ga[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kDdU; ++u) {
+            const uint32_t i = base + u * THREADS;
+            bool pending = false;
+            if (i < n) {
+                const uint32_t fp = dd_fp(m[u], fmask);
+                const uint32_t nearest = min(min(v[u].x ^ fp, v[u].y ^ fp), min(v[u].z ^ fp, v[u].w ^ fp));
+                const uint32_t occ = (v[u].x >> 31) + (v[u].y >> 31) + (v[u].z >> 31) + (v[u].w >> 31); // a prefix
+                uint32_t cur = 1u;
+                if (nearest > imask && occ < 4u)
+                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(cur) : "r"(ga[u] + 4u * occ), "r"(0u), "r"(fp | i)
+                                 : "memory");
+                if (cur == 0u)
+                    ++mine;
+                else
+                    pending = true;
+            }
+            const uint32_t pb = __ballot_sync(0xffffffffu, pending);
+            if (pending) q[qn + __popc(pb & lt)] = static_cast<uint16_t>(i);
+            qn += __popc(pb);
+        }
+        __syncwarp();
+        while (qn >= 32u) { // a full warp of pending keys
+            qn -= 32u;
+            const uint32_t i = q[qn + lane];
+            __syncwarp();
+            settle(i);
+        }
+    }
+    if (lane < qn) settle(q[lane]);
+}
+
 // One CTA per bucket: the distinct count of its n mixed keys through a
 // shared-memory set of 32-bit slots.  A slot holds (fingerprint | index of
 // the key in the bucket); the keys themselves are staged in shared memory
@@ -701,11 +800,12 @@ __global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* of
                                                           const unsigned long long* keys, const uint32_t* bucket_doc,
                                                           unsigned long long* term_count, unsigned int* overflow,
                                                           uint32_t slots, uint32_t kcap, uint32_t nbuf,
-                                                          uint32_t fp_test_mask) {
+                                                          uint32_t fp_test_mask, uint32_t fast) {
     extern __shared__ __align__(16) uint8_t dd_smem[];
     uint4* s_grp = reinterpret_cast<uint4*>(dd_smem);                                          // slots / 4 groups
     unsigned long long* s_buf = reinterpret_cast<unsigned long long*>(dd_smem + 4ull * slots); // nbuf x kcap keys
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_buf + static_cast<uint64_t>(nbuf) * kcap); // nbuf mbarriers
+    uint16_t* s_queue = reinterpret_cast<uint16_t*>(s_bar + nbuf); // per warp: kDdQueue pending key indices
     if (threadIdx.x == 0) {
         for (uint32_t j = 0; j < nbuf; ++j) mbar_init(&s_bar[j], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -747,7 +847,14 @@ __global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* of
         bool stuck = ib > 28; // (a bucket of > 2^28 keys: the wave is recounted)
         if (!stuck) {
             const uint32_t imask = (1u << ib) - 1u;
-            if (st)
+            if (st && fast)
+                dd_bucket_fast<THREADS, true>(n, sg, G - 1u, imask, ~imask & fp_test_mask,
+                                              static_cast<uint32_t>(__cvta_generic_to_shared(s_buf + b * kcap + (o0 & 1u))),
+                                              nullptr, s_queue, mine, stuck);
+            else if (fast && n <= 65536u) // (queue entries are 16-bit key indices)
+                dd_bucket_fast<THREADS, false>(n, sg, G - 1u, imask, ~imask & fp_test_mask, 0u, keys + o0, s_queue, mine,
+                                               stuck);
+            else if (st)
                 dd_bucket<THREADS, true>(n, sg, G - 1u, imask, ~imask & fp_test_mask,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(s_buf + b * kcap + (o0 & 1u))),
                                          nullptr, mine, stuck);
@@ -1285,12 +1392,22 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             // set + key staging buffer(s) + mbarrier(s) (a wave's kcap is capped so this fits)
             uint32_t nbuf = 1; // key staging buffers (A/B knob COBS_PC_DD_NBUF = 1 / 2; 1: more CTAs per SM, faster)
             if (const char* e = std::getenv("COBS_PC_DD_NBUF")) nbuf = std::atoi(e) == 1 ? 1u : 2u;
-            auto dd_smem = [&](uint64_t slots, uint64_t kcap) { return static_cast<size_t>(4 * slots + nbuf * (8 * kcap + 8)); };
+            const uint64_t dd_queue = 2ull * kDdQueue * ((dd512 ? 512 : 256) / 32); // the warps' pending-key queues
+            auto dd_smem = [&](uint64_t slots, uint64_t kcap) {
+                return static_cast<size_t>(4 * slots + nbuf * (8 * kcap + 8) + dd_queue);
+            };
             COBS_CUDA(cudaFuncSetAttribute(dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
             // tests narrow the fingerprints to force accidental matches (COBS_PC_FP_MASK, e.g. 0x30000)
             const uint32_t fp_test_mask = std::getenv("COBS_PC_FP_MASK")
                                               ? static_cast<uint32_t>(std::strtoul(std::getenv("COBS_PC_FP_MASK"), nullptr, 0))
                                               : 0xffffffffu;
+            // straight-line first probes in the dedup (A/B knob COBS_PC_DD_FAST=0: the per-key probe loop)
+            const char* df_env = std::getenv("COBS_PC_DD_FAST");
+            const uint32_t dd_fast = !(df_env && df_env[0] == '0');
+            // keys staged in shared memory by the bulk-copy engine, or (COBS_PC_DD_STAGE=0) read from
+            // global memory one step ahead: half the shared memory per CTA, twice the warps per SM
+            const char* ds_env = std::getenv("COBS_PC_DD_STAGE");
+            const bool dd_stage = !(ds_env && ds_env[0] == '0');
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
                 if (!wv.nchunk) continue;
@@ -1327,12 +1444,12 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
                     d_docs.as<PcDoc>() + wv.doc0, d_sup_doc[b].as<uint32_t>(), wv.nsup, d_off[b].as<uint32_t>(),
                     d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
-                const uint64_t kcap = std::min<uint64_t>(wv.kcap, ((227 * 1024 - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
+                const uint64_t kcap = !dd_stage ? 0 : std::min<uint64_t>(wv.kcap, ((227 * 1024 - dd_queue - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
                 dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dd512 ? 512 : 256,
                         dd_smem(wv.slots, kcap), st>>>(
                     d_off[b].as<uint32_t>(), wv.nbuck, d_keys.as<unsigned long long>(), d_bdoc[b].as<uint32_t>(),
                     d_tc.as<unsigned long long>(), reinterpret_cast<unsigned int*>(flags + 1),
-                    static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf, fp_test_mask);
+                    static_cast<uint32_t>(wv.slots), static_cast<uint32_t>(kcap), nbuf, fp_test_mask, dd_fast);
                 COBS_CUDA(cudaEventRecord(ev_done[b], st));
                 COBS_CUDA(cudaGetLastError());
             }
