@@ -345,7 +345,21 @@ struct PcArgs {
     unsigned long long* bad;  // non-ACGT windows without canonicalisation (byte path needed)
     uint32_t* chunk_sup;      // two-level: per (chunk, super-bucket) key counts [chunk][kSup], or null
     const uint8_t* symtab;    // SB > 0: byte -> symbol index (256 entries)
+    unsigned long long* work; // the wave's work counters (zeroed): [0] histogram chunks, [1] scatter chunks, [2] super-buckets
 };
+
+// Persistent CTAs take their next unit (chunk, super-bucket) from a global
+// counter instead of striding by the grid: the grids below ask for more
+// CTAs than fit an SM (registers), and the histogram pass shares the SMs
+// with the previous wave's kernels, so a fixed stride left the late CTAs'
+// whole share to run on mostly empty SMs.  Call with all threads; includes
+// the barrier that ends the previous unit's use of shared memory.
+__device__ __forceinline__ uint64_t pc_next_unit(unsigned long long* counter, unsigned long long* s_slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s_slot = atomicAdd(counter, 1ull);
+    __syncthreads();
+    return *s_slot;
+}
 
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
     return shift >= 64 ? 0u : static_cast<uint32_t>(mix_code(code) >> shift);
@@ -409,9 +423,11 @@ __global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
     __shared__ uint32_t s_doc;
     __shared__ unsigned long long s_bad;
     __shared__ uint8_t s_sym[256];
+    __shared__ unsigned long long s_unit;
     if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        __syncthreads();
+    for (;;) {
+        const uint64_t c = pc_next_unit(p.work + 0, &s_unit);
+        if (c >= p.nchunks) break;
         if (threadIdx.x == 0) {
             s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
             s_bad = 0;
@@ -471,9 +487,11 @@ __global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_
     __shared__ uint32_t s_cnt[kSup], s_base[kSup];
     __shared__ uint32_t s_doc;
     __shared__ uint8_t s_sym[256];
+    __shared__ unsigned long long s_unit;
     if (SB) s_sym[threadIdx.x] = p.symtab[threadIdx.x]; // (256 threads)
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        __syncthreads();
+    for (;;) {
+        const uint64_t c = pc_next_unit(p.work + 1, &s_unit);
+        if (c >= p.nchunks) break;
         if (threadIdx.x == 0) s_doc = pc_chunk_doc(p.docs, p.ndocs, c);
         __syncthreads();
         const PcDoc D = p.docs[s_doc];
@@ -504,16 +522,18 @@ constexpr uint32_t kFinPer = kFinTile / 256; // keys per thread per tile
 __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs, const uint32_t* sup_doc,
                                                                uint64_t nsup, const uint32_t* off,
                                                                const unsigned long long* keys_a,
-                                                               unsigned long long* keys_b) {
+                                                               unsigned long long* keys_b, unsigned long long* work) {
     constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
     __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB];
     __shared__ unsigned long long s_sorted[kFinTile];
     __shared__ uint8_t s_lb[kFinTile];
-    for (uint64_t g = blockIdx.x; g < nsup; g += gridDim.x) {
+    __shared__ unsigned long long s_unit;
+    for (;;) {
+        const uint64_t g = pc_next_unit(work, &s_unit);
+        if (g >= nsup) break;
         const PcDoc D = docs[sup_doc[g]];
         const uint32_t sbs = pc_super_shift(D), bps = 1u << sbs;
         const uint64_t b_lo = D.bucket0 + ((g - D.sb0) << sbs);
-        __syncthreads();
         for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] = off[b_lo + t];
         const uint32_t k0 = off[b_lo], k1 = off[b_lo + bps];
         // (loading the next tile's keys while this one is placed: 122
@@ -1344,7 +1364,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             size_t tmp_bytes = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
                                           static_cast<int>(max_nbuck + 1), st);
-            std::vector<std::pair<BufView*, size_t>> plan{{&d_flags, 16 * std::max<size_t>(pw.size(), 1)},
+            std::vector<std::pair<BufView*, size_t>> plan{{&d_flags, 64 * std::max<size_t>(pw.size(), 1)}, // per wave: bad, overflow, 3 work counters
                                                        {&d_docs, sizeof(PcDoc) * std::max<size_t>(pd.size(), 1)}};
             for (int b = 0; b < (overlap ? 2 : 1); ++b) {
                 plan.push_back({&d_chunk_sup[b], 4ull * kSup * max_nchunk});
@@ -1369,7 +1389,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             COBS_CUDA(cudaEventRecord(ek0, st));
             if (!pd.empty())
                 COBS_CUDA(cudaMemcpyAsync(d_docs.ptr, pd.data(), sizeof(PcDoc) * pd.size(), cudaMemcpyHostToDevice, st));
-            COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 16 * std::max<size_t>(pw.size(), 1), st));
+            COBS_CUDA(cudaMemsetAsync(d_flags.ptr, 0, 64 * std::max<size_t>(pw.size(), 1), st));
             cudaStream_t hs = st;
             if (overlap) COBS_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
             struct HsGuard {
@@ -1404,16 +1424,17 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             // straight-line first probes in the dedup (A/B knob COBS_PC_DD_FAST=0: the per-key probe loop)
             const char* df_env = std::getenv("COBS_PC_DD_FAST");
             const uint32_t dd_fast = !(df_env && df_env[0] == '0');
-            // keys staged in shared memory by the bulk-copy engine, or (COBS_PC_DD_STAGE=0) read from
-            // global memory one step ahead: half the shared memory per CTA, twice the warps per SM
+            // keys read from global memory one step ahead, or (A/B knob COBS_PC_DD_STAGE=1) staged in shared
+            // memory by the bulk-copy engine: twice the shared memory per CTA, half the warps per SM
+            // (C3 count kernels 1,173 vs 1,246 ms)
             const char* ds_env = std::getenv("COBS_PC_DD_STAGE");
-            const bool dd_stage = !(ds_env && ds_env[0] == '0');
+            const bool dd_stage = ds_env && ds_env[0] == '1';
             for (size_t i = 0; i < pw.size(); ++i) {
                 const PcWave& wv = pw[i];
                 if (!wv.nchunk) continue;
                 const int b = overlap ? static_cast<int>(i & 1) : 0;
                 const uint32_t nd = static_cast<uint32_t>(wv.d1 - wv.d0);
-                unsigned long long* flags = d_flags.as<unsigned long long>() + 2 * i;
+                unsigned long long* flags = d_flags.as<unsigned long long>() + 8 * i;
                 PcArgs pa{};
                 pa.a = wa;
                 pa.docs = d_docs.as<PcDoc>() + wv.doc0;
@@ -1424,6 +1445,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 pa.bad = flags;
                 pa.chunk_sup = d_chunk_sup[b].as<uint32_t>();
                 pa.symtab = d_symtab.as<uint8_t>();
+                pa.work = flags + 2;
                 const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(148 * 6, wv.nchunk)));
                 // histogram side (buffers b are free once wave i-2's dedup is done)
                 COBS_CUDA(cudaStreamWaitEvent(hs, ev_done[b], 0));
@@ -1443,7 +1465,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 scat<<<grid, 256, 0, st>>>(pa, d_sup_cur[b].as<uint32_t>());
                 pc_scatter_final_kernel<<<static_cast<unsigned>(std::min<uint64_t>(148 * 8, wv.nsup)), 256, 0, st>>>(
                     d_docs.as<PcDoc>() + wv.doc0, d_sup_doc[b].as<uint32_t>(), wv.nsup, d_off[b].as<uint32_t>(),
-                    d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>());
+                    d_keys_a.as<unsigned long long>(), d_keys.as<unsigned long long>(), flags + 4);
                 const uint64_t kcap = !dd_stage ? 0 : std::min<uint64_t>(wv.kcap, ((227 * 1024 - dd_queue - 4 * wv.slots) / nbuf / 8 - 1) & ~1ull);
                 dedup<<<static_cast<unsigned>(std::min<uint64_t>(148 * 64, wv.nbuck)), dd512 ? 512 : 256,
                         dd_smem(wv.slots, kcap), st>>>(
@@ -1454,9 +1476,9 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                 COBS_CUDA(cudaGetLastError());
             }
             g_timing.count_waves = static_cast<uint32_t>(pw.size());
-            std::vector<uint64_t> flags(2 * pw.size());
+            std::vector<uint64_t> flags(8 * pw.size());
             if (!pw.empty())
-                COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 16 * pw.size(), cudaMemcpyDeviceToHost, st));
+                COBS_CUDA(cudaMemcpyAsync(flags.data(), d_flags.ptr, 64 * pw.size(), cudaMemcpyDeviceToHost, st));
             COBS_CUDA(cudaEventRecord(ek1, st));
             COBS_CUDA(cudaStreamSynchronize(st));
             {
@@ -1470,11 +1492,11 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             d_keys_a.release();
             g_timing.ms_count_free = ms_since(t_free);
             bool byte_windows = !oversize.empty() || sym_bits; // symbol-coded windows hash their bytes in the fill
-            for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[2 * i] != 0;
+            for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[8 * i] != 0;
             if (!byte_windows) fill_rpt = kFillRunsDna;
             const auto t_recount = std::chrono::steady_clock::now();
             for (size_t i = 0; i < pw.size(); ++i)
-                if (flags[2 * i] || (flags[2 * i + 1] & 0xffffffffull)) { // recount this wave exactly
+                if (flags[8 * i] || (flags[8 * i + 1] & 0xffffffffull)) { // recount this wave exactly
                     COBS_CUDA(cudaMemsetAsync(d_tc.as<unsigned long long>() + pw[i].d0, 0, 8 * (pw[i].d1 - pw[i].d0), st));
                     hashset_count(pw[i].d0, pw[i].d1);
                     ++g_timing.count_fallback_waves;
