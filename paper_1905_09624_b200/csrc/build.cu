@@ -417,8 +417,16 @@ __device__ __forceinline__ void pc_windows(const WinArgs& a, const PcDoc& D, uin
     }
 }
 
+// (min CTAs per SM, A/B: 4 -> 55-56 registers; 5 -> 48 registers: C3 count
+// 1,158 vs 1,116 ms; 6 -> 40 registers and spills: 1,241 ms)
+#ifndef COBS_PC_HIST_MINB
+#define COBS_PC_HIST_MINB 4
+#endif
+#ifndef COBS_PC_SCAT_MINB
+#define COBS_PC_SCAT_MINB 4
+#endif
 template <int QC, int SB = 0>
-__global__ void __launch_bounds__(256) pc_hist_kernel(PcArgs p) {
+__global__ void __launch_bounds__(256, COBS_PC_HIST_MINB) pc_hist_kernel(PcArgs p) {
     __shared__ uint32_t s_hist[kPcHist];
     __shared__ uint32_t s_doc;
     __shared__ unsigned long long s_bad;
@@ -483,7 +491,7 @@ __global__ void pc_super_init_kernel(const PcDoc* docs, uint32_t ndocs, const ui
 }
 
 template <int QC, int SB = 0>
-__global__ void __launch_bounds__(256) pc_scatter_super_kernel(PcArgs p, uint32_t* sup_cursor) {
+__global__ void __launch_bounds__(256, COBS_PC_SCAT_MINB) pc_scatter_super_kernel(PcArgs p, uint32_t* sup_cursor) {
     __shared__ uint32_t s_cnt[kSup], s_base[kSup];
     __shared__ uint32_t s_doc;
     __shared__ uint8_t s_sym[256];
@@ -979,7 +987,10 @@ constexpr uint32_t kFillRunsDna = 16;
 // every window of a document -> k bits of its slab column; one thread per
 // `rpt` consecutive runs of one document (run_prefix counts those spans)
 template <int QC>
-__global__ void __launch_bounds__(256) slab_fill_kernel(WinArgs a, const SlabDoc* docs,
+#ifndef COBS_FILL_MINB
+#define COBS_FILL_MINB 3
+#endif
+__global__ void __launch_bounds__(256, COBS_FILL_MINB) slab_fill_kernel(WinArgs a, const SlabDoc* docs,
                                                         const uint64_t* run_prefix, uint32_t ndocs,
                                                         unsigned int* slab, uint32_t rpt) {
     const uint32_t q = QC ? QC : a.q;
