@@ -281,6 +281,14 @@ int cobs_gpu_build_timing_ex(double* ms_h2d, double* ms_count, double* ms_fill, 
  * of the workspace's cudaMalloc and cudaFree calls (both inside ms_count). */
 int cobs_gpu_build_timing_count(double* ms_kernels, double* ms_alloc, double* ms_free);
 
+/* Releases the device memory the library keeps between calls: the build's
+ * count workspace (<= 17 GB: two key buffers and per-wave arrays, kept so
+ * that repeated builds skip their cudaMalloc / cudaFree; COBS_BUILD_CACHE=0
+ * frees it after every build).  The library also releases it by itself when
+ * one of its own device allocations runs out of memory.  Returns the bytes
+ * released. */
+uint64_t cobs_gpu_trim(void);
+
 void cobs_gpu_free(void* p);
 
 /* ---- file front ends ------------------------------ */

@@ -634,6 +634,12 @@ def last_build_timing() -> Tuple[float, float, float]:
     return a.value, b.value, c.value
 
 
+def trim() -> int:
+    """Release the device memory kept between calls (the build's count
+    workspace); returns the bytes released."""
+    return int(N.lib.cobs_gpu_trim())
+
+
 def last_build_timing_ex() -> dict:
     """ms of the last build's legs: h2d, count, fill, d2h, total."""
     v = [C.c_double() for _ in range(5)]

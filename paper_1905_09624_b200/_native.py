@@ -105,6 +105,7 @@ SIGNATURES = {
                                         C.POINTER(C.c_double)]),
     "cobs_gpu_build_timing_ex": (C.c_int, [C.POINTER(C.c_double)] * 5),
     "cobs_gpu_build_timing_count": (C.c_int, [C.POINTER(C.c_double)] * 3),
+    "cobs_gpu_trim": (C.c_uint64, []),
     "cobs_gpu_free": (None, [vp]),
     "cobs_gpu_index_synth_c5": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                           C.c_double, C.c_double, C.c_int, C.POINTER(vp),

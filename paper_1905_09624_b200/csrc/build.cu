@@ -25,6 +25,7 @@
 //               the distinct ones.
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1098,6 +1099,53 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 
 const BuildTiming& last_build_timing() { return g_timing; }
 
+// The partitioned count's workspace (two key buffers of <= 8 GB each and the
+// per-wave arrays) is kept between builds: cudaFree of these buffers took
+// 6-20 ms usually but 100-600 ms on some builds (profiles/r2/session5:
+// free_timing.log, the `free=` column of the A/B logs), cudaMalloc 2-130 ms.
+// One workspace per process, handed to one build at a time (a concurrent
+// build allocates its own and frees it); released by cobs_gpu_trim(), by
+// DevBuf::reserve when an allocation of this library runs out of memory, or
+// with COBS_BUILD_CACHE=0 after every build.
+struct CountWorkspace {
+    DevBuf keys, keys_a, small;
+    int device = -1;
+    size_t bytes() const { return keys.bytes + keys_a.bytes + small.bytes; }
+};
+namespace {
+std::mutex g_ws_mu;
+CountWorkspace* g_ws = nullptr; // (leaked at exit: the runtime may be gone when statics die)
+std::unique_ptr<CountWorkspace> acquire_count_ws(int device) {
+    std::unique_ptr<CountWorkspace> ws;
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        ws.reset(g_ws);
+        g_ws = nullptr;
+    }
+    if (ws && ws->device != device) ws.reset(); // (its buffers are freed)
+    if (!ws) {
+        ws = std::make_unique<CountWorkspace>();
+        ws->device = device;
+    }
+    return ws;
+}
+void release_count_ws(std::unique_ptr<CountWorkspace> ws) {
+    const char* e = std::getenv("COBS_BUILD_CACHE");
+    if (e && e[0] == '0') return; // freed here
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (!g_ws) g_ws = ws.release();
+}
+} // namespace
+size_t trim_device_caches() {
+    std::unique_ptr<CountWorkspace> ws;
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        ws.reset(g_ws);
+        g_ws = nullptr;
+    }
+    return ws ? ws->bytes() : 0;
+}
+
 std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint64_t* seg_off,
                                                 uint64_t n_segs, const uint64_t* doc_segs,
                                                 const std::vector<std::string>& names, const Params& P,
@@ -1367,7 +1415,8 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             const auto t_alloc = std::chrono::steady_clock::now();
             const char* ov_env = std::getenv("COBS_PC_OVERLAP");
             const bool overlap = !(ov_env && ov_env[0] == '0');
-            DevBuf d_keys, d_keys_a, d_small;
+            std::unique_ptr<CountWorkspace> cws = acquire_count_ws(device);
+            DevBuf &d_keys = cws->keys, &d_keys_a = cws->keys_a, &d_small = cws->small;
             d_keys.reserve(8 * max_keys + 16); // (+16: the dedup's 16-byte staged copies may read one key past the end)
             d_keys_a.reserve(8 * max_keys);
             // the per-wave arrays: views into one allocation (one cudaMalloc / cudaFree instead of ~20)
@@ -1499,8 +1548,10 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
             }
             g_timing.ms_count_sync = ms_since(t_count0);
             const auto t_free = std::chrono::steady_clock::now();
-            d_keys.release(); // before any recount needs the memory
-            d_keys_a.release();
+            // (a recount that runs out of memory gets it back through DevBuf::reserve)
+            if (cws->bytes() <= 16 * kPcWaveKeys + (1ull << 30))
+                release_count_ws(std::move(cws)); // kept for the next build
+            cws.reset();
             g_timing.ms_count_free = ms_since(t_free);
             bool byte_windows = !oversize.empty() || sym_bits; // symbol-coded windows hash their bytes in the fill
             for (size_t i = 0; i < pw.size(); ++i) byte_windows |= flags[8 * i] != 0;

@@ -461,6 +461,8 @@ int cobs_gpu_build_timing_count(double* ms_kernels, double* ms_alloc, double* ms
     return COBS_OK;
 }
 
+uint64_t cobs_gpu_trim(void) { return cobsg::trim_device_caches(); }
+
 void cobs_gpu_free(void* p) { std::free(p); }
 
 int cobs_gpu_index_synth_c5(uint64_t seed, uint64_t n_docs, uint64_t block_size, double median,

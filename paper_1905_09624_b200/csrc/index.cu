@@ -22,7 +22,12 @@ void DevBuf::reserve(size_t n) {
     ptr = nullptr;
     bytes = 0;
     if (n == 0) return;
-    COBS_CUDA(cudaMalloc(&ptr, n));
+    cudaError_t e = cudaMalloc(&ptr, n);
+    if (e == cudaErrorMemoryAllocation && trim_device_caches() > 0) { // the cached count workspace may be in the way
+        cudaGetLastError();
+        e = cudaMalloc(&ptr, n);
+    }
+    COBS_CUDA(e);
     bytes = n;
 }
 void DevBuf::release() {

@@ -27,6 +27,11 @@ struct DevBuf {
     ~DevBuf();
 };
 
+// Frees the device memory the library keeps between calls (the build's count
+// workspace, see build.cu); DevBuf::reserve calls it and retries once when
+// cudaMalloc runs out of memory.  Returns the bytes released.
+size_t trim_device_caches();
+
 struct PinnedBuf {
     void* ptr = nullptr;
     size_t bytes = 0;

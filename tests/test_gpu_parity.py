@@ -495,6 +495,28 @@ def test_count_partitioned_vs_hashset(gpu):
                               COBS_PC_WAVE_KEYS=150000) == want
 
 
+def test_count_workspace_cache_and_trim(gpu):
+    """The partitioned count keeps its workspace between builds (cobs_gpu_trim
+    releases it; COBS_BUILD_CACHE=0 never keeps it); the files do not depend
+    on whether a build starts from a cached, larger or smaller workspace."""
+    rng = random.Random(5)
+    small = [(b"s%02d" % i, [rand(rng, 3000)]) for i in range(10)]
+    large = [(b"l%02d" % i, [rand(rng, 120000)]) for i in range(10)]
+    params = cb.IndexParams(q=31, canonical=True, block_size=8)
+    want_s = O.build_image(small, q=31, canonical=True, block_size=8, kind=1)
+    want_l = O.build_image(large, q=31, canonical=True, block_size=8, kind=1)
+    cb.trim()
+    assert cb.trim() == 0
+    assert _build_env(small, params, cb.KIND_COMPACT) == want_s
+    assert _build_env(large, params, cb.KIND_COMPACT) == want_l   # grows the cached workspace
+    assert _build_env(small, params, cb.KIND_COMPACT) == want_s   # reuses a larger one
+    kept = cb.trim()
+    assert kept >= 16 * sum(len(d[1][0]) - 30 for d in large)     # two 8-byte key buffers
+    assert cb.trim() == 0
+    assert _build_env(large, params, cb.KIND_COMPACT, COBS_BUILD_CACHE=0) == want_l
+    assert cb.trim() == 0
+
+
 def test_count_partitioned_symbol_codes(gpu):
     """Raw-byte corpora over a small alphabet (<= 32 byte values, q <= 12)
     take the partitioned count with 5-bit symbol codes (SymRoller): the same

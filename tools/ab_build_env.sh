@@ -12,4 +12,5 @@ for v in "$@"; do
     last="$def"
   fi
   env $envs COBS_BUILD_DEBUG=1 python tools/config_runs.py ${CFG:-c3} --build-only --repeat 3 --out /tmp/ab.json 2>&1 | grep -E "count .* ms" | tail -2 | cut -c1-120
+  python -c "import json; b=json.load(open('/tmp/ab.json'))[0]['build']; print('  last build: count %.1f fill %.1f total %.1f ms' % (b['ms_count'], b['ms_fill'], b['ms_total_call']))"
 done
