@@ -279,4 +279,8 @@ inline std::unique_ptr<GpuIndexView> merge_classic(const GpuIndexView& a, const 
     return std::make_unique<GpuIndexView>(h);
 }
 
+// Releases the device memory kept between calls (the build's count workspace,
+// cobs_gpu_trim); returns the bytes released.
+inline uint64_t trim() { return cobs_gpu_trim(); }
+
 } // namespace cobs_b200
