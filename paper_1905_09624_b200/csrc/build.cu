@@ -533,9 +533,8 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
                                                                const unsigned long long* keys_a,
                                                                unsigned long long* keys_b, unsigned long long* work) {
     constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
-    __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB];
+    __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB], s_off[kMaxB];
     __shared__ unsigned long long s_sorted[kFinTile];
-    __shared__ uint8_t s_lb[kFinTile];
     __shared__ unsigned long long s_unit;
     for (;;) {
         const uint64_t g = pc_next_unit(work, &s_unit);
@@ -577,7 +576,11 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
                         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                         if (threadIdx.x >= static_cast<uint32_t>(o)) incl += y;
                     }
-                    if (c0 + threadIdx.x < bps) s_start[c0 + threadIdx.x] = carry + incl - v;
+                    if (c0 + threadIdx.x < bps) {
+                        s_start[c0 + threadIdx.x] = carry + incl - v;
+                        // sorted position i of the tile -> its place in keys_b (mod 2^32)
+                        s_off[c0 + threadIdx.x] = s_cur[c0 + threadIdx.x] - (carry + incl - v);
+                    }
                     carry += __shfl_sync(0xffffffffu, incl, 31);
                 }
             }
@@ -585,14 +588,13 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
 #pragma unroll
             for (uint32_t u = 0; u < kFinPer; ++u)
                 if (threadIdx.x + u * blockDim.x < n) {
-                    const uint32_t pos = s_start[lr[u] & 0xffu] + (lr[u] >> 8);
-                    s_sorted[pos] = kv[u];
-                    s_lb[pos] = static_cast<uint8_t>(lr[u] & 0xffu);
+                    s_sorted[s_start[lr[u] & 0xffu] + (lr[u] >> 8)] = kv[u];
                 }
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) { // consecutive i -> consecutive addresses per run
-                const uint32_t lb = s_lb[i];
-                keys_b[s_cur[lb] + (i - s_start[lb])] = s_sorted[i];
+                const unsigned long long k = s_sorted[i];            // (its bucket again from the key itself)
+                const uint32_t lb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(k >> D.shift)) & (bps - 1u);
+                keys_b[s_off[lb] + i] = k;
             }
             __syncthreads();
             for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cur[t] += s_cnt[t];
@@ -739,6 +741,10 @@ __device__ __forceinline__ void dd_bucket(uint32_t n, uint32_t sg, uint32_t gmas
 #define COBS_DD_U 1
 #endif
 constexpr int kDdU = COBS_DD_U;
+#ifndef COBS_DD_LOAD
+#define COBS_DD_LOAD 4
+#endif
+constexpr uint32_t kDdLoadNum = COBS_DD_LOAD; // set slots >= kDdLoadNum / 2 x keys where the launch's slots allow
 constexpr uint32_t kDdQueue = 32u * kDdU + 32u; // pending keys a warp can hold (u16 indices)
 template <int THREADS, bool SMEM>
 __device__ __forceinline__ void dd_bucket_fast(uint32_t n, uint32_t sg, uint32_t gmask, uint32_t imask, uint32_t fmask,
@@ -864,7 +870,7 @@ __global__ void __launch_bounds__(THREADS) pc_dedup_fp_kernel(const uint32_t* of
         }
         const uint32_t ib = max(16, 32 - __clz(static_cast<int>(n - 1)));
         uint32_t G = 64; // groups: load <= 2/3 where the launch's slots allow
-        while (G * 4 < n + n / 2 && G * 4 < slots) G <<= 1;
+        while (G * 4 < kDdLoadNum * n / 2 && G * 4 < slots) G <<= 1;
         for (uint32_t j = threadIdx.x; j < G; j += THREADS) s_grp[j] = make_uint4(0u, 0u, 0u, 0u);
         const bool st = staged(o0, n);
         if (st) {
