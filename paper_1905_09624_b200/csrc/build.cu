@@ -362,8 +362,20 @@ __device__ __forceinline__ uint64_t pc_next_unit(unsigned long long* counter, un
     return *s_slot;
 }
 
+#ifndef COBS_PC_MIX_LIGHT
+#define COBS_PC_MIX_LIGHT 1
+#endif
+// the partitioned count's key of a code: a bijection whose top bits (bucket),
+// low bits (set group) and bits 32..46 (fingerprint) all depend on the whole code
+__device__ __forceinline__ uint64_t pc_mix(uint64_t z) {
+    if (COBS_PC_MIX_LIGHT) { // one multiply + one fold (A/B vs the splitmix64 finaliser: C3 count 1,038 vs 1,057 ms, C4 211 vs 217)
+        z *= 0x9E3779B97F4A7C15ULL;
+        return z ^ (z >> 32);
+    }
+    return mix_code(z);
+}
 __device__ __forceinline__ uint32_t pc_bucket(uint64_t code, uint32_t shift) {
-    return shift >= 64 ? 0u : static_cast<uint32_t>(mix_code(code) >> shift);
+    return shift >= 64 ? 0u : static_cast<uint32_t>(pc_mix(code) >> shift);
 }
 
 constexpr int kSymBits = 5;                  // symbol codes: <= 32 distinct byte values, q <= 12
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(256, COBS_PC_SCAT_MINB) pc_scatter_super_kerne
         __syncthreads();
         pc_windows<QC, SB>(p.a, D, r0, r1, [&](bool dna, uint64_t code) {
             if (!dna) return;
-            const uint64_t m = mix_code(code);
+            const uint64_t m = pc_mix(code);
             const uint32_t sb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(m >> D.shift)) >> sbs;
             p.keys[s_base[sb] + atomicAdd(&s_cnt[sb], 1u)] = m;
         }, s_sym);
@@ -526,7 +538,10 @@ __global__ void __launch_bounds__(256, COBS_PC_SCAT_MINB) pc_scatter_super_kerne
 // a tile of kFinTile keys at a time: counting-sorted by bucket in shared
 // memory, then each bucket's run of the tile written with coalesced stores
 // (whole sectors, no read-modify-write of partially written ones).
-constexpr uint32_t kFinTile = 4096;
+#ifndef COBS_FIN_TILE
+#define COBS_FIN_TILE 4096
+#endif
+constexpr uint32_t kFinTile = COBS_FIN_TILE;
 constexpr uint32_t kFinPer = kFinTile / 256; // keys per thread per tile
 __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs, const uint32_t* sup_doc,
                                                                uint64_t nsup, const uint32_t* off,
@@ -1778,13 +1793,15 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
         COBS_CUDA(cudaMemcpyAsync(d_up.ptr, unit_prefix.data(), 8 * unit_prefix.size(), cudaMemcpyHostToDevice, st));
         COBS_CUDA(cudaEventRecord(e2, st));
         auto fk = q == 31 ? slab_fill_kernel<31> : slab_fill_kernel<0>;
+        // (a grid of one resident round, 148 x 3 CTAs, measured slower: C3 fill 1,076 vs 1,017 ms, C4 273 vs 254)
+        const uint64_t fill_grid = 148 * 16;
         for (const Batch& B : batches) {
             for (size_t i = B.wave0; i < B.wave0 + B.nwaves; ++i) {
                 const Wave& wv = waves[i];
                 COBS_CUDA(cudaMemsetAsync(d_slab.as<unsigned int>() + wv.w_lo, 0, 4 * (wv.w_hi - wv.w_lo), st));
                 const uint64_t runs = run_prefix[wv.rp0 + wv.ndocs];
                 if (runs > 0)
-                    fk<<<static_cast<unsigned>(std::min<uint64_t>(148 * 16, (runs + 255) / 256)), 256, 0, st>>>(
+                    fk<<<static_cast<unsigned>(std::min<uint64_t>(fill_grid, (runs + 255) / 256)), 256, 0, st>>>(
                         wa, d_sdocs.as<SlabDoc>() + wv.doc0, d_rp.as<uint64_t>() + wv.rp0,
                         static_cast<uint32_t>(wv.ndocs), d_slab.as<unsigned int>(), fill_rpt);
                 COBS_CUDA(cudaGetLastError());
