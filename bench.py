@@ -545,7 +545,8 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
     """docs/s of index construction on a config's full corpus, generated in
     HBM: one warm-up build (reported as `cold`: the first build of a process
     also pays the first touch of its fresh key buffers), then the median of
-    3 builds.  `docs_per_s_kernels` counts the count + fill passes (sequences
+    5 builds (on power-capped boxes about one fill pass in four runs 20-50 %
+    long, profiles/r2/session5/ab_fillnoise.log).  `docs_per_s_kernels` counts the count + fill passes (sequences
     in HBM -> finished, queryable matrix), `docs_per_s_call` the whole call."""
     import torch
     cfg = synth.CONFIGS[name]
@@ -559,7 +560,7 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
     torch.cuda.synchronize()
     runs = []
     index_bytes = 0
-    for rep in range(4):
+    for rep in range(6):
         view, _ = cb.build_device(dev.data_ptr(), seg_off, np.arange(cfg.n_docs + 1), names, params, cfg.kind,
                                   device=device, seqs_on_device=True)
         runs.append(cb.last_build_timing_ex())
