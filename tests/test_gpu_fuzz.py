@@ -50,7 +50,9 @@ def test_fuzz_build_and_query(gpu, it):
     # small waves -- the corpora are below its size threshold, so forced
     knobs = {"COBS_COUNT_PARTITION": "1", "COBS_PC_TARGET": str(rng.choice([64, 300, 4096])),
              "COBS_PC_FP_MASK": rng.choice(["0xffffffff", "0x30000", "0x0"]),
-             "COBS_PC_WAVE_KEYS": str(rng.choice([2000, 1 << 30]))}
+             "COBS_PC_WAVE_KEYS": str(rng.choice([2000, 1 << 30])),
+             # dedup: straight-line first probes or the per-key loop, keys from global memory or staged
+             "COBS_PC_DD_FAST": rng.choice(["1", "1", "0"]), "COBS_PC_DD_STAGE": rng.choice(["0", "0", "1"])}
     saved = {v: os.environ.get(v) for v in knobs}
     os.environ.update(knobs)
     try:

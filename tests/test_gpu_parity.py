@@ -485,6 +485,13 @@ def test_count_partitioned_vs_hashset(gpu):
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_SLOTS_CAP=256) == want
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_TARGET=512) == want
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_NBUF=2, COBS_PC_DEDUP_THREADS=512) == want
+            # dedup variants: keys staged in shared memory (one / two buffers), the per-key probe loop
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_STAGE=1) == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_STAGE=1, COBS_PC_DD_NBUF=2,
+                              COBS_PC_DEDUP_THREADS=512) == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_FAST=0) == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_FAST=0, COBS_PC_DD_STAGE=1) == want
+            assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_DD_STAGE=1, COBS_PC_FP_MASK=0x30000) == want
             # 2-bit fingerprints: most probes meet accidental matches and compare whole keys
             assert _build_env(corpus, params, cb.KIND_COMPACT, COBS_PC_FP_MASK=0x30000) == want
             # waves of <= 150,000 keys: many waves, and "big"/"polyA" exceed one
