@@ -383,11 +383,26 @@ constexpr int kSymBits = 5;                  // symbol codes: <= 32 distinct byt
 #define COBS_PC_PACKED 1
 #endif
 constexpr bool kPcPacked = COBS_PC_PACKED != 0; // 2-bit codes rolled 16 bases at a time (roll_range_packed)
-constexpr uint32_t kSupLog2 = 5;             // two-level scatter: <= 32 super-buckets per document (A/B: 64 and 256 slower)
+#ifndef COBS_PC_SUPLOG2
+#define COBS_PC_SUPLOG2 4
+#endif
+constexpr uint32_t kSupLog2 = COBS_PC_SUPLOG2; // two-level scatter: <= 16 super-buckets per document (A/B, C3 count: 8 -> 1,211 ms,
+                                               // 16 -> 998, 32 -> 1,052; 64 and 256 slower still): fewer runs = more lanes of a
+                                               // warp's store in one 128-byte line
 constexpr uint32_t kSup = 1u << kSupLog2;
+#ifndef COBS_PC_BPSLOG2
+#define COBS_PC_BPSLOG2 4
+#endif
+// log2(buckets per super-bucket) of a document with 2^lg buckets: <= kSup
+// super-buckets, and >= 2^COBS_PC_BPSLOG2 buckets in each where the document has that many
+__host__ __device__ __forceinline__ uint32_t pc_super_shift_lg(uint32_t lg) {
+    const uint32_t a = lg - (lg < kSupLog2 ? lg : kSupLog2);
+    constexpr uint32_t kBps = COBS_PC_BPSLOG2;
+    const uint32_t b = kBps == 0u ? 0u : (lg < kBps ? lg : kBps);
+    return a > b ? a : b;
+}
 __device__ __forceinline__ uint32_t pc_super_shift(const PcDoc& D) { // bucket >> this = super-bucket
-    const uint32_t lg = 64u - D.shift;                               // log2(nbk)
-    return lg - min(lg, kSupLog2);
+    return pc_super_shift_lg(64u - D.shift);                         // (64 - shift = log2(nbk))
 }
 
 // chunk c -> its document (last i with docs[i].chunk0 <= c, skipping empty ones)
@@ -548,7 +563,8 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
                                                                const unsigned long long* keys_a,
                                                                unsigned long long* keys_b, unsigned long long* work) {
     constexpr uint32_t kMaxB = kPcHist / kSup > 128 ? kPcHist / kSup : 128; // buckets per super-bucket
-    __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_start[kMaxB], s_off[kMaxB];
+    __shared__ uint32_t s_cur[kMaxB], s_cnt[kMaxB], s_off[kMaxB];
+    __shared__ uint16_t s_start[kMaxB]; // (< kFinTile)
     __shared__ unsigned long long s_sorted[kFinTile];
     __shared__ unsigned long long s_unit;
     for (;;) {
@@ -566,7 +582,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
             for (uint32_t t = threadIdx.x; t < bps; t += blockDim.x) s_cnt[t] = 0;
             __syncthreads();
             unsigned long long kv[kFinPer];
-            uint32_t lr[kFinPer]; // bucket (low 8 bits) | rank within the tile's bucket << 8
+            uint32_t lr[kFinPer]; // bucket (low 12 bits) | rank within the tile's bucket << 12
 #pragma unroll
             for (uint32_t u = 0; u < kFinPer; ++u) {
                 const uint32_t i = threadIdx.x + u * blockDim.x;
@@ -577,7 +593,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
                 lr[u] = 0;
                 if (threadIdx.x + u * blockDim.x < n) {
                     const uint32_t lb = (D.shift >= 64 ? 0u : static_cast<uint32_t>(kv[u] >> D.shift)) & (bps - 1u);
-                    lr[u] = lb | (atomicAdd(&s_cnt[lb], 1u) << 8);
+                    lr[u] = lb | (atomicAdd(&s_cnt[lb], 1u) << 12);
                 }
             }
             __syncthreads();
@@ -592,7 +608,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
                         if (threadIdx.x >= static_cast<uint32_t>(o)) incl += y;
                     }
                     if (c0 + threadIdx.x < bps) {
-                        s_start[c0 + threadIdx.x] = carry + incl - v;
+                        s_start[c0 + threadIdx.x] = static_cast<uint16_t>(carry + incl - v);
                         // sorted position i of the tile -> its place in keys_b (mod 2^32)
                         s_off[c0 + threadIdx.x] = s_cur[c0 + threadIdx.x] - (carry + incl - v);
                     }
@@ -603,7 +619,7 @@ __global__ void __launch_bounds__(256) pc_scatter_final_kernel(const PcDoc* docs
 #pragma unroll
             for (uint32_t u = 0; u < kFinPer; ++u)
                 if (threadIdx.x + u * blockDim.x < n) {
-                    s_sorted[s_start[lr[u] & 0xffu] + (lr[u] >> 8)] = kv[u];
+                    s_sorted[s_start[lr[u] & 0xfffu] + (lr[u] >> 12)] = kv[u];
                 }
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) { // consecutive i -> consecutive addresses per run
@@ -1418,7 +1434,7 @@ std::unique_ptr<DeviceIndex> build_device_index(const uint8_t* seqs, const uint6
                     D.sb0 = static_cast<uint32_t>(wv.nsup);
                     D.tpr = kPcRunsPerThread;
                     pd.push_back(D);
-                    wv.nsup += std::min<uint64_t>(nbk, kSup);
+                    wv.nsup += nbk >> pc_super_shift_lg(static_cast<uint32_t>(__builtin_ctzll(nbk)));
                     wv.keys += W;
                     wv.nbuck += nbk;
                     wv.nchunk += (D.run_hi - D.run_lo + kPcRuns - 1) / kPcRuns;
