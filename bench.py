@@ -605,8 +605,8 @@ def bench_build_cfg(cb, synth, name: str, device: int) -> dict:
         "count": {"bound": "issue/latency (rolling, per-key scattered stores, the dedup probe loop), not HBM",
                   "design_bytes": count_bytes, "achieved_gbs": count_bytes / (c / 1e3) / 1e9,
                   "peak_gbs": peak, "frac": count_bytes / (c / 1e3) / 1e9 / peak,
-                  "ncu": "profiles/r2/session5/launch_build_c3_s5f.csv (C3 launch list, serialised: hist 153, "
-                         "super scatter 332, final 265, dedup 287 ms; scatter / final / dedup = 0.30 / 0.66 / 0.31 "
+                  "ncu": "profiles/r2/session5/launch_build_c3_s5g.csv (C3 launch list, serialised: hist 151, "
+                         "super scatter 222, final 339, dedup 289 ms; scatter / final / dedup = 0.45 / 0.52 / 0.31 "
                          "of the HBM peak on their own design bytes); per-kernel ncu details: "
                          "profiles/r2/session5/ncu/, dedup_fast_u1_details.csv"},
         "fill": {"bound": "issue (IMAD pipe: XXH64's 19 64-bit multiplies per window), not HBM",
